@@ -1,0 +1,458 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix
+(not against the oracle itself).  CPU only.
+
+Each test names the PAPER.md passage (P:<line>) or closed form it checks.
+A plausible slip anywhere in oracle/abft_oracle.c (dropped alpha/beta term,
+wrong sign, transposed axis, wrong neighbour direction, wrong BC, wrong
+injection point, wrong correction algebra, rollback not restoring) fails at
+least one test here.
+"""
+import math
+import os
+import random
+import struct
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from abft_inputs import (Fault, Problem, fault_schedule, field_power, field_u0,
+                         make_problem, splitmix64, splitmix64_numpy, uniform)
+from oracle import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold_lines(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return [l.split("#")[0].strip() for l in f if l.split("#")[0].strip()]
+
+
+# ----------------------------------------------------------- generators
+
+def test_splitmix64_known_values():
+    want = [int(v, 16) for v in _gold_lines("splitmix64_seed0.txt")]
+    got = splitmix64(0, 0, 0, len(want)).numpy().view(np.uint64).tolist()
+    assert got == want
+
+
+def test_splitmix64_torch_equals_numpy_wraparound():
+    a = splitmix64(12345, 4, 1000, 4096).numpy().view(np.uint64)
+    b = splitmix64_numpy(12345, 4, 1000, 4096)
+    assert (a == b).all()
+
+
+def test_uniform_f32_grid_and_range():
+    u = uniform(0, 1, 100000, "f32", 323.0, 343.0).numpy()
+    assert u.dtype == np.float32 and u.min() >= 323.0 and u.max() < 343.0
+    v = uniform(0, 1, 1000, "f32").numpy().astype(np.float64)
+    assert np.all(v * 2 ** 24 == np.floor(v * 2 ** 24))     # multiples of 2^-24
+
+
+def test_fault_schedules_follow_recipes():
+    f1 = fault_schedule(make_problem("cfg1"))
+    assert len(f1) == 1 and f1[0].sweep == 10 and 0 <= f1[0].bit <= 30
+    f2 = fault_schedule(make_problem("cfg2"))
+    assert [f.sweep for f in f2] == list(range(10, 101, 10))
+    f3 = fault_schedule(make_problem("cfg3"))
+    assert len(f3) == 20 and len({f.sweep for f in f3}) == 20
+    f4 = fault_schedule(make_problem("cfg4"))
+    assert len(f4) == 32
+    for f in f4:   # one per 128-plane slab per 50-sweep block
+        assert sum(1 for g in f4 if g.z // 128 == f.z // 128 and
+                   (g.sweep - 1) // 50 == (f.sweep - 1) // 50) == 1
+    f5 = fault_schedule(make_problem("cfg5"))
+    assert len(f5) == 50 and len({(f.sweep, f.z) for f in f5}) == 50
+    assert max(f.bit for f in f5) <= 63
+
+
+# ------------------------------------------------------------ fault hook
+
+def test_flip_ieee_layout():
+    for line in _gold_lines("ieee_flip.txt"):
+        dt, val, bit, want = line.split()
+        if dt == "f32":
+            a = np.array([float(val)], np.float32)
+            O.flip(a, 0, int(bit))
+            assert a.view(np.uint32)[0] == int(want, 16)
+        else:
+            a = np.array([float(val)], np.float64)
+            O.flip(a, 0, int(bit))
+            assert a.view(np.uint64)[0] == int(want, 16)
+
+
+def test_flip_is_an_involution():
+    rng = np.random.default_rng(0)
+    a = rng.random(64).astype(np.float32)
+    b = a.copy()
+    for k in range(64):
+        O.flip(b, k, k % 32)
+        assert b[k] != a[k] or np.isnan(b[k])
+        O.flip(b, k, k % 32)
+    assert (a.view(np.uint32) == b.view(np.uint32)).all()
+
+
+# -------------------------------------------------------- checksums Eqs. 2-3
+
+def test_checksums_worked_example():
+    g = {l.split(":")[0]: l.split(":")[1] for l in _gold_lines("checksum_2x2.txt")}
+    rows = [[float(v) for v in r.split()] for r in g["grid_rows_y"].split("|")]
+    p = Problem("t", 2, 2, 1, "f32", [(0, 0, 0, 1.0)], [])
+    A, B = O.checksums(O.OProblem(p), np.array(rows, np.float32))
+    assert A[0].tolist() == [float(v) for v in g["a"].split()]
+    assert B[0].tolist() == [float(v) for v in g["b"].split()]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_checksums_brute_force(dtype):
+    p = Problem("t", 13, 7, 3, dtype, [(0, 0, 0, 1.0)], [])
+    rng = np.random.default_rng(1)
+    u = rng.random((3, 7, 13)).astype(np.float32 if dtype == "f32" else np.float64)
+    A, B = O.checksums(O.OProblem(p), u)
+    for z in range(3):
+        for x in range(13):
+            want = math.fsum(float(u[z, y, x]) for y in range(7))
+            assert abs(A[z, x] - want) <= 1e-15 * abs(want)
+            if dtype == "f32":
+                assert A[z, x] == want          # exact: fp64 sum of few fp32 values
+        for y in range(7):
+            want = math.fsum(float(u[z, y, x]) for x in range(13))
+            assert abs(B[z, y] - want) <= 1e-15 * abs(want)
+        assert abs(math.fsum(A[z]) - math.fsum(B[z])) < 1e-12   # both = plane total
+
+
+# ---------------------------------------------------------------- sweep Eq. 1
+
+def _exact_sweep(u, pts, bc, nz, ny, nx, g=0):
+    """Brute-force Eq. 1 in exact rational arithmetic (tiny grids)."""
+    def r(c, n):
+        if 0 <= c < n:
+            return c
+        if bc == 0:
+            return 0 if c < 0 else n - 1
+        if bc == 1:
+            return c % n
+        return None
+    out = np.empty((nz, ny, nx), dtype=object)
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                s = Fraction(0)
+                for (di, dj, dk, w) in pts:
+                    zz, yy, xx = r(z + dk, nz), r(y + dj, ny), r(x + di, nx)
+                    v = Fraction(g) if None in (zz, yy, xx) else Fraction(float(u[zz, yy, xx]))
+                    s += Fraction(w) * v
+                out[z, y, x] = s
+    return out
+
+
+def test_sweep_identity_is_copy():
+    p = Problem("t", 9, 5, 2, "f32", [(0, 0, 0, 1.0)], [])
+    u = np.random.default_rng(2).random((2, 5, 9)).astype(np.float32)
+    out = O.sweep(O.OProblem(p), u)
+    assert (out.view(np.uint32) == u.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+def test_sweep_dyadic_exact_brute_force(bc):
+    # dyadic weights, integer data < 2^10: every fp32 operation is exact, so the
+    # oracle must equal exact rational Eq. 1 incl. the BC of P:289-292.
+    pts = [(0, 0, 0, 0.25), (-1, 0, 0, 0.125), (1, 0, 0, 0.0625), (0, 1, 0, 0.125),
+           (0, -1, 0, 0.1875), (0, 0, 1, 0.125), (0, 0, -1, 0.125)]
+    g = 7.0 if bc == 3 else 0.0
+    p = Problem("t", 6, 5, 4, "f32", pts, [], bc=bc, bc_value=g)
+    u = np.random.default_rng(3).integers(0, 1024, (4, 5, 6)).astype(np.float32)
+    out = O.sweep(O.OProblem(p), u)
+    want = _exact_sweep(u, pts, bc, 4, 5, 6, g)
+    assert all(Fraction(float(out[i])) == want[i] for i in np.ndindex(out.shape))
+
+
+def test_sweep_four_point_paper_example_checkerboard():
+    # S = {(0,-1,.25), (-1,0,.25), (1,0,.25), (0,1,.25)}: with periodic BC
+    # every neighbour of a +1 cell of a checkerboard is -1, so the sweep negates it.
+    line = [l for l in _gold_lines("paper_parameters.txt") if l.startswith("four_point")][0]
+    pts = []
+    for t in line.split(":", 1)[1].split():
+        i, j, w = t.strip("()").split(",")
+        pts.append((int(i), int(j), 0, float(w)))
+    p = Problem("t", 8, 6, 1, "f32", pts, [], bc=1)
+    x, y = np.meshgrid(np.arange(8), np.arange(6))
+    u = np.where((x + y) % 2 == 0, 1.0, -1.0).astype(np.float32)[None]
+    out = O.sweep(O.OProblem(p), u)
+    assert (out == -u).all()
+
+
+def test_sweep_uniform_fixed_point_and_vertical_direction():
+    # weights summing to 1, C = 0: a uniform field is a fixed point
+    pts = [(0, 0, 0, 0.5), (-1, 0, 0, 0.125), (1, 0, 0, 0.125), (0, -1, 0, 0.125),
+           (0, 1, 0, 0.125)]
+    p = Problem("t", 5, 4, 2, "f32", pts, [])
+    u = np.full((2, 4, 5), 3.25, np.float32)
+    assert (O.sweep(O.OProblem(p), u) == u).all()
+    # t = z+1 and b = z-1 (HotSpot, Q22): u = f(z) layered; only (0,0,+1) weighted
+    p = Problem("t", 3, 3, 4, "f32", [(0, 0, 1, 1.0)], [])
+    u = np.arange(4, dtype=np.float32)[:, None, None] * np.ones((4, 3, 3), np.float32)
+    out = O.sweep(O.OProblem(p), u)
+    assert out[:, 0, 0].tolist() == [1.0, 2.0, 3.0, 3.0]    # clamped at the top
+
+
+def test_sweep_sources_hotspot_closed_form():
+    # uniform T, weights summing to 1: out = T + sdc*P + ct*amb exactly in the
+    # FMA chain when T*w terms are exact (T = 256, dyadic weights 0.5/0.125/...)
+    pts = [(0, 0, 0, 0.5), (-1, 0, 0, 0.125), (1, 0, 0, 0.125), (0, -1, 0, 0.0625),
+           (0, 1, 0, 0.0625), (0, 0, 1, 0.0625), (0, 0, -1, 0.0625)]
+    srcs = [(0.5, True, 0.0), (0.25, False, 8.0)]
+    p = Problem("t", 4, 4, 3, "f32", pts, srcs)
+    P = np.full((3, 4, 4), 2.0, np.float32)
+    u = np.full((3, 4, 4), 256.0, np.float32)
+    out = O.sweep(O.OProblem(p, [P]), u)
+    assert (out == 256.0 + 0.5 * 2.0 + 0.25 * 8.0).all()
+
+
+# ------------------------------------------------------ Theorem 1 (prediction)
+
+def _fsum_checksums(u):
+    nz, ny, nx = u.shape
+    A = np.array([[math.fsum(float(v) for v in u[z, :, x]) for x in range(nx)] for z in range(nz)])
+    B = np.array([[math.fsum(float(v) for v in u[z, y, :]) for y in range(ny)] for z in range(nz)])
+    return A, B
+
+
+def _random_stencil(rng, k, symmetric=False):
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+    rng.shuffle(offs)
+    sel = offs[:k]
+    return [(di, dj, dk, float(rng.uniform(0.01, 0.3))) for (di, dj, dk) in sel]
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+@pytest.mark.parametrize("seed", range(4))
+def test_theorem1_prediction_equals_brute_force_checksums(bc, seed):
+    # Theorem 1: interpolated a', b' == checksums of the swept grid,
+    # for arbitrary (asymmetric) radius-1 stencils, every BC, 3D (Q6), fp64.
+    rng = random.Random(seed)
+    pts = _random_stencil(rng, rng.randint(3, 27))
+    p = Problem("t", 7, 6, 5, "f64", pts, [(0.3, True, 0.0), (0.2, False, 1.5)],
+                bc=bc, bc_value=0.75)
+    nrng = np.random.default_rng(seed)
+    u = nrng.random((5, 6, 7))
+    P = nrng.random((5, 6, 7))
+    op = O.OProblem(p, [P])
+    A, B = O.checksums(op, u)
+    PA, PB = O.predict(op, A, B, u)
+    u1 = O.sweep(op, u)
+    A1, B1 = _fsum_checksums(u1)
+    assert np.max(np.abs(PA - A1) / np.abs(A1)) < 1e-12
+    assert np.max(np.abs(PB - B1) / np.abs(B1)) < 1e-12
+
+
+def test_theorem1_negative_control_dropped_boundary_terms():
+    # Dropping alpha/beta (u := 0 in the ledger) must break Theorem 1 for an
+    # asymmetric clamp stencil -- shows the pin above is sensitive --
+    # while for a mirror-symmetric clamp stencil or periodic BC the simplified
+    # Eqs. 6-7 (alpha = beta = 0) hold.
+    nrng = np.random.default_rng(7)
+    u = nrng.random((3, 8, 9))
+    zeros = np.zeros_like(u)
+    asym = [(0, 0, 0, 0.4), (-1, 0, 0, 0.3), (1, 0, 0, 0.1), (0, 1, 0, 0.15), (0, -1, 0, 0.05)]
+    sym = [(0, 0, 0, 0.6), (-1, 0, 0, 0.1), (1, 0, 0, 0.1), (0, 1, 0, 0.1), (0, -1, 0, 0.1)]
+    for pts, bc, must_hold in [(asym, 0, False), (sym, 0, True), (asym, 1, True)]:
+        op = O.OProblem(Problem("t", 9, 8, 3, "f64", pts, [], bc=bc))
+        A, B = O.checksums(op, u)
+        PA, PB = O.predict(op, A, B, zeros)
+        A1, B1 = _fsum_checksums(O.sweep(op, u))
+        gap = max(np.max(np.abs(PA - A1) / A1), np.max(np.abs(PB - B1) / B1))
+        assert (gap < 1e-12) == must_hold, (pts, bc, gap)
+
+
+def test_theorem1_dyadic_exact_equality():
+    # dyadic workload: every operation exact => predicted == actual exactly
+    pts = [(0, 0, 0, 0.5), (-1, 0, 0, 0.125), (1, 0, 0, 0.0625), (0, -1, 0, 0.125),
+           (0, 1, 0, 0.0625), (0, 0, 1, 0.0625), (0, 0, -1, 0.0625)]
+    p = Problem("t", 16, 16, 4, "f32", pts, [])
+    op = O.OProblem(p)
+    u = np.random.default_rng(5).integers(0, 1024, (4, 16, 16)).astype(np.float32)
+    A, B = O.checksums(op, u)
+    PA, PB = O.predict(op, A, B, u)
+    A1, B1 = O.checksums(op, O.sweep(op, u))
+    assert (PA == A1).all() and (PB == B1).all()
+
+
+# ------------------------------------------------------ detection (Thm 2)
+
+def test_flag_rule_closed_cases():
+    # fig.detect: flagged iff |pred/act - 1| > eps (fp64, Q7, Q24)
+    assert O.flag(1.0 + 2e-5, 1.0, 1e-5) == 1
+    assert O.flag(1.0 + 5e-6, 1.0, 1e-5) == 0
+    assert O.flag(1.0 - 2e-5, 1.0, 1e-5) == 1
+    assert O.flag(0.0, 0.0, 1e-5) == 0
+    assert O.flag(1e-300, 0.0, 1e-5) == 1
+    assert O.flag(float("nan"), 1.0, 1e-5) == 1
+    assert O.flag(1.0, float("nan"), 1e-5) == 1
+    assert O.flag(1.0, float("inf"), 1e-5) == 1
+    assert O.flag(-3.0, 3.0, 1e-5) == 1
+
+
+def _cfg1_like(**kw):
+    return make_problem("cfg1", **kw)
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("cfg1", {}),
+    ("cfg2", dict(nx=64, ny=48, nz=6, sweeps=40)),
+    ("cfg3", dict(nx=40, ny=33, nz=5, sweeps=30, mode=2, delta=10)),
+    ("cfg5", dict(nx=24, ny=20, nz=6, sweeps=20, mode=1)),
+    ("cfg5", dict(nx=24, ny=20, nz=6, sweeps=20)),
+])
+def test_no_false_positives_error_free(name, kw):
+    # Theorem 2 and "no false-positives" at eps
+    p = make_problem(name, **kw)
+    op = O.OProblem(p, [field_power(p).numpy()] if p.power else [])
+    r = O.run(op, field_u0(p).numpy(), p.sweeps)
+    assert r["stats"]["detections"] == 0 and r["status"] == 0 and r["records"] == []
+
+
+def _clean_states(p, op, u0, s):
+    q = p.replace(mode=0)
+    oq = O.OProblem(q, op._fields)
+    return O.run(oq, u0, s)["u"]
+
+
+def test_detection_closed_form_and_location_cfg1():
+    # For one flip at sweep s: delta = flipped - clean is exact; since the
+    # prediction equals the clean checksum up to ~1e-8, the B (row) entry is
+    # flagged iff |delta| > eps*|S + delta| (S clean row sum), same for A.
+    # Every flip flagged in both vectors must be located at the injected cell
+    # and corrected (Eq. 8).
+    p = _cfg1_like()
+    op = O.OProblem(p)
+    u0 = field_u0(p).numpy()
+    s = 10
+    clean = _clean_states(p, op, u0, s)
+    rng = random.Random(11)
+    checked = 0
+    for trial in range(120):
+        y, x, bit = rng.randrange(64), rng.randrange(64), rng.randrange(31)
+        cv = np.array([clean[0, y, x]], np.float32)
+        fv = cv.copy()
+        O.flip(fv, 0, bit)
+        d = float(fv[0]) - float(cv[0])
+        Srow = math.fsum(float(v) for v in clean[0, y, :])
+        Scol = math.fsum(float(v) for v in clean[0, :, x])
+        mb = abs(d) / abs(Srow + d) if math.isfinite(d) else math.inf
+        ma = abs(d) / abs(Scol + d) if math.isfinite(d) else math.inf
+        if 0.9 * p.eps < mb < 1.1 * p.eps or 0.9 * p.eps < ma < 1.1 * p.eps:
+            continue                               # ambiguous band
+        r = O.run(op, u0, s, [Fault(s, 0, y, x, bit)])
+        expect_b, expect_a = mb > p.eps, ma > p.eps
+        if not (expect_a or expect_b):
+            assert r["records"] == []
+        else:
+            rec = r["records"][0]
+            assert rec["sweep"] == s and rec["z"] == 0
+            assert (rec["nflag_b"] == 1) == expect_b and (rec["nflag_a"] == 1) == expect_a
+            if expect_a and expect_b:
+                assert (rec["y"], rec["x"]) == (y, x) and rec["status"] == O.REC_CORRECTED
+                assert abs(rec["corrected"] - float(cv[0])) <= 1e-5 * abs(float(cv[0]))
+                # fig.correction: corrected = (vx + vy) / 2, in the dtype
+                assert rec["corrected"] == float(np.float32((rec["vx"] + rec["vy"]) / 2.0))
+                assert rec["vx"] != rec["vy"] or rec["corrected"] == np.float32(rec["vx"])
+        checked += 1
+    assert checked > 80
+
+
+def test_paper_bits_0_12_undetected_high_bits_detected():
+    # flips in bits 0..12 are never detected (64x64, eps = 1e-5);
+    # bits 13..31 are mostly detected and corrected.
+    par = {l.split(":")[0]: l.split(":")[1].strip() for l in _gold_lines("paper_parameters.txt")}
+    lo, hi = (int(v) for v in par["undetected_bits_fp32"].split("-"))
+    p = _cfg1_like(sweeps=6)
+    op = O.OProblem(p)
+    u0 = field_u0(p).numpy()
+    rng = random.Random(3)
+    for bit in list(range(lo, hi + 1)) + list(range(20, 32)):
+        det = 0
+        for t in range(12):
+            f = Fault(rng.randint(1, 6), 0, rng.randrange(64), rng.randrange(64), bit)
+            r = O.run(op, u0, 6, [f])
+            det += r["stats"]["detections"]
+        if bit <= hi:
+            assert det == 0, bit
+        else:
+            assert det == 12, bit
+
+
+# ------------------------------------------------------------- correction
+
+def test_correction_dyadic_is_bitwise_exact():
+    # dyadic workload: predicted == actual exactly (sweeps 1-4), so the
+    # re-summed Eq. 8 restores the clean value bitwise and the whole run equals
+    # the fault-free run bitwise.
+    pts = [(0, 0, 0, 0.5), (-1, 0, 0, 0.125), (1, 0, 0, 0.125), (0, -1, 0, 0.125),
+           (0, 1, 0, 0.125)]
+    p = Problem("t", 32, 32, 2, "f32", pts, [], eps=1e-5, mode=1, sweeps=4)
+    op = O.OProblem(p)
+    u0 = np.random.default_rng(9).integers(0, 1024, (2, 32, 32)).astype(np.float32)
+    ref = O.run(op, u0, 4)
+    rng = random.Random(4)
+    for t in range(40):
+        f = Fault(rng.randint(1, 4), rng.randrange(2), rng.randrange(32), rng.randrange(32),
+                  rng.randint(13, 30))
+        r = O.run(op, u0, 4, [f])
+        if r["stats"]["corrected"] == 1:
+            assert (r["u"].view(np.uint32) == ref["u"].view(np.uint32)).all()
+            assert r["stats"]["detections"] == 1     # repaired checksums: no later flags
+
+
+def test_correction_literal_form_fails_on_exponent_flip():
+    # "if the bit-flips occur in the last bits of the exponent, the error
+    # causes an overflow in the checksums" -- the literal fig.correction form
+    # a' - (a - u) loses the value when u ~ 1e38; the re-summed form (Q11) not.
+    p = _cfg1_like(sweeps=10)
+    u0 = field_u0(p).numpy()
+    clean = _clean_states(p, O.OProblem(p), u0, 10)[0, 20, 30]
+    f = [Fault(10, 0, 20, 30, 30)]
+    lit = O.run(O.OProblem(p.replace(correction_form=1)), u0, 10, f)["records"][0]
+    res = O.run(O.OProblem(p), u0, 10, f)["records"][0]
+    assert abs(res["corrected"] - clean) / clean < 1e-5
+    assert not abs(lit["corrected"] - clean) / clean < 1e-2
+
+
+# ---------------------------------------------------------------- offline
+
+def test_offline_rollback_erases_error_bitwise():
+    # P:913 / P:867: checkpoint + recompute "completely" erases detected errors.
+    p = make_problem("cfg3", nx=48, ny=40, nz=6, sweeps=30, mode=2, delta=10, nfaults=3)
+    P = field_power(p).numpy()
+    op = O.OProblem(p, [P])
+    u0 = field_u0(p).numpy()
+    ref = O.run(op, u0, 30)
+    faults = [Fault(4, 2, 7, 9, 27), Fault(15, 5, 39, 0, 30), Fault(30, 0, 0, 47, 31)]
+    r = O.run(op, u0, 30, faults)
+    assert r["stats"]["rollbacks"] == 3 and r["status"] == 0
+    assert (r["u"].view(np.uint32) == ref["u"].view(np.uint32)).all()
+    assert {(x["sweep"], x["z"]) for x in r["records"]} >= {(10, 2), (20, 5), (30, 0)}
+
+
+def test_offline_persistent_error():
+    # a fault that strikes again during the recomputation (second armed copy)
+    p = make_problem("cfg3", nx=32, ny=32, nz=4, sweeps=10, mode=2, delta=5)
+    op = O.OProblem(p, [field_power(p).numpy()])
+    f = [Fault(3, 1, 5, 5, 30), Fault(3, 1, 5, 5, 30)]
+    r = O.run(op, field_u0(p).numpy(), 10, f)
+    assert r["status"] == 3 and r["stats"]["persistent"] == 1
+    assert any(x["status"] == O.REC_PERSISTENT for x in r["records"])
+
+
+def test_offline_interpolation_matches_direct_after_delta_sweeps():
+    # algo.offline.inteprolation: applying Theorem 1 delta times to
+    # the checkpoint checksums reproduces the direct checksums (fp64, 27-pt).
+    p = make_problem("cfg5", nx=12, ny=10, nz=5, sweeps=8)
+    op = O.OProblem(p)
+    u = field_u0(p).numpy()
+    A, B = O.checksums(op, u)
+    for t in range(8):
+        A, B = O.predict(op, A, B, u)
+        u = O.sweep(op, u)
+    A1, B1 = _fsum_checksums(u)
+    assert np.max(np.abs(A - A1) / A1) < 1e-12 and np.max(np.abs(B - B1) / B1) < 1e-12
