@@ -72,13 +72,13 @@ def splitmix64_numpy(seed: int, stream: int, start: int, count: int) -> np.ndarr
 
 
 def uniform(seed: int, stream: int, n: int, dtype: str, lo: float = 0.0,
-            hi: float = 1.0, device="cpu", chunk: int = 1 << 26) -> torch.Tensor:
-    """n draws U[lo,hi) of `dtype` ('f32' | 'f64') in linear-index order."""
+            hi: float = 1.0, device="cpu", chunk: int = 1 << 26, start: int = 0) -> torch.Tensor:
+    """draws [start, start+n) of U[lo,hi) of `dtype` ('f32' | 'f64'), linear-index order."""
     tdt = torch.float32 if dtype == "f32" else torch.float64
     out = torch.empty(n, dtype=tdt, device=device)
     for s in range(0, n, chunk):
         c = min(chunk, n - s)
-        r = splitmix64(seed, stream, s, c, device)
+        r = splitmix64(seed, stream, start + s, c, device)
         if dtype == "f32":
             u = _lsr(r, 40).to(torch.float64) * (2.0 ** -24)
         else:
@@ -204,16 +204,25 @@ def make_problem(name: str, **overrides) -> Problem:
     return _cfg(name).replace(**overrides)
 
 
-def field_u0(p: Problem, device="cpu") -> torch.Tensor:
+def field_u0(p: Problem, device="cpu", z0: int = 0, zc: Optional[int] = None) -> torch.Tensor:
+    """Initial field, layers [z0, z0 + zc) of the global domain (a z-slab)."""
+    zc = p.nz - z0 if zc is None else zc
     lo, hi = p.init
-    return uniform(p.seed, 1, p.cells, p.dtype, lo, hi, device).view(p.nz, p.ny, p.nx)
+    n = zc * p.ny * p.nx
+    return uniform(p.seed, 1, n, p.dtype, lo, hi, device,
+                   start=z0 * p.ny * p.nx).view(zc, p.ny, p.nx)
 
 
-def field_power(p: Problem, device="cpu") -> Optional[torch.Tensor]:
+def field_power(p: Problem, device="cpu", z0: int = 0,
+                zc: Optional[int] = None) -> Optional[torch.Tensor]:
+    """HotSpot power field (source of C), layers [z0, z0 + zc)."""
     if p.power is None:
         return None
+    zc = p.nz - z0 if zc is None else zc
     lo, hi = p.power
-    return uniform(p.seed, 2, p.cells, p.dtype, lo, hi, device).view(p.nz, p.ny, p.nx)
+    n = zc * p.ny * p.nx
+    return uniform(p.seed, 2, n, p.dtype, lo, hi, device,
+                   start=z0 * p.ny * p.nx).view(zc, p.ny, p.nx)
 
 
 class _Draw:

@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the ABFT-protected stencil hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+One "step" is one protected sweep of the whole workload: K1 (Eq. 1 sweep +
+actual checksums, Eqs. 2-3) and K2 (Theorem 1 prediction, compare, locate,
+correct) over every z-layer, with the config's scheduled bit-flips.  The
+default workload is BASELINE.json configs[3] (cfg4): HotSpot3D 7-point,
+1024^3 fp32, online ABFT, 200 sweeps, one flip per 128-layer slab per 50
+sweeps, z-partitioned over N GPUs (one process per GPU, NCCL halo).  Inputs
+(4 GiB per array) are larger than L2, so no flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  `value` = protected GCell-updates/s of the
+whole job (max time over ranks); `e2e` = the same through the C-ABI with
+host buffers (pinned H2D of u0 and P, init, K sweeps, D2H of the field);
+`roofline` = the dominant kernel K1 against the measured HBM copy peak;
+`cpu_baseline` = the CPU oracle on a bounded sample (rank 0, N = 1).
+`--impl reference` times the oracle as it stands (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+try:
+    _CORES = len(os.sched_getaffinity(0))
+except AttributeError:
+    _CORES = os.cpu_count() or 1
+os.environ.setdefault("OMP_NUM_THREADS", str(_CORES))
+
+import torch  # noqa: E402
+
+from abft_inputs import fault_schedule, field_power, field_u0, make_problem  # noqa: E402
+
+METRIC = "protected GCell-updates/s at 1/2/4/8 B200, %HBM roofline, ABFT overhead %"
+UNIT = "GCell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-layers", type=int, default=0, help="oracle sample layers (0 = auto)")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return a
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured", mp
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed regions (B200_PROFILING.md recipe)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: str):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "-i", index,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        self.windows = []
+
+    def mark(self):
+        return time.time()
+
+    def window(self, t0, t1):
+        self.windows.append((t0, t1))
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [l.strip().split(", ") for l in self.f.read().splitlines() if l.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for k, n in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(n)
+        # samples under load: the upper half of the clock distribution while timing
+        load = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def timed(stream, fn):
+    """device time (ms) of fn() on `stream` with CUDA events, synchronised both sides."""
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def shift(faults, k):
+    from abft_inputs import Fault
+    return [Fault(f.sweep + k, f.z, f.y, f.x, f.bit) for f in faults]
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(a):
+    from paper_1909_00709_b200 import abft
+    world, rank, local = dist_env()
+    if a.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    p = make_problem(a.config)
+    if p.nz % world:
+        raise SystemExit(f"nz={p.nz} not divisible by {world} ranks")
+    zc = p.nz // world
+    z0 = rank * zc
+    cells_local = p.nx * p.ny * zc
+    cells_global = p.cells
+    K, W = a.steps, a.warmup
+    stream = torch.cuda.Stream(dev)
+    u0 = field_u0(p, dev, z0, zc)
+    P = field_power(p, dev, z0, zc)
+    faults = fault_schedule(p, K)
+    kw = dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    idx = vis.split(",")[local] if vis and vis.split(",")[local].isdigit() else str(local)
+    clocks = Clocks(idx)
+
+    def protected_run(mode, with_faults, prof=False):
+        st = abft.from_problem(p, u0, P, device=dev, stream=stream, mode=mode, **kw)
+        if with_faults:
+            st.set_faults(shift(faults, W))
+        st.step(W)
+        barrier(world)
+        if prof:
+            st.profile(True)
+        l0 = st.launches
+        t0 = clocks.mark()
+        ms = timed(stream, lambda: st.step(K))
+        clocks.window(t0, clocks.mark())
+        out = dict(ms=ms, launches=st.launches - l0)
+        if prof:
+            out["prof"] = st.profile_read()
+        out["stats"] = st.stats()
+        out["status"] = st.status()
+        st.destroy()
+        return out
+
+    with torch.cuda.stream(stream):
+        rA = protected_run(abft.ABFT_MODE_ONLINE, True, prof=True)    # headline: flips on
+        rB = protected_run(abft.ABFT_MODE_ONLINE, False, prof=True)   # error-free protected
+        rC = protected_run(abft.ABFT_MODE_NONE, False, prof=True)     # unprotected sweep
+    ck = clocks.stop()
+    tA = max_over_ranks(rA["ms"], world)
+    tB = max_over_ranks(rB["ms"], world)
+    tC = max_over_ranks(rC["ms"], world)
+    value = cells_global * K / (tA * 1e-3) / 1e9
+    # roofline of the dominant kernel K1 (protected, checksums fused): algorithmic
+    # bytes = (field read + source read + field write) * cells of the launch
+    esz = 4 if p.dtype == "f32" else 8
+    nfield = sum(1 for s in p.sources if s[1])
+    bytes_cell = (2 + nfield) * esz
+    prof = rB["prof"]
+    k1_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
+    k2_ms = prof["k2_ms"] / max(1, prof["k2_launches"])
+    k1_gbs = bytes_cell * cells_local / (k1_ms * 1e-3) / 1e9
+    k1_ms_unprot = rC["prof"]["k1_ms"] / max(1, rC["prof"]["k1_launches"])
+    peak, peak_kind, mp = peaks()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    launches = sum_over_ranks(rA["launches"], world)
+
+    # end to end through the C-ABI with host buffers
+    e2e = None
+    if not a.no_e2e:
+        u0h = u0.cpu().pin_memory()
+        Ph = P.cpu().pin_memory() if P is not None else None
+        outh = torch.empty_like(u0h).pin_memory()
+        Pd = torch.empty_like(P) if P is not None else None
+
+        def job():
+            if Pd is not None:
+                Pd.copy_(Ph, non_blocking=True)
+            st = abft.from_problem(p, u0h, Pd, device=dev, stream=stream, **kw)
+            st.set_faults(faults)
+            st.step(K)
+            st.read_field(outh)
+            s = st.stats()
+            st.destroy()
+            return s
+
+        with torch.cuda.stream(stream):
+            job()   # warm the caching allocator
+            barrier(world)
+            te = timed(stream, job)
+        te = max_over_ranks(te, world)
+        h2d = u0h.numel() * esz + (Ph.numel() * esz if Ph is not None else 0)
+        d2h = outh.numel() * esz + 72 + 80 * 4096
+        e2e = {"value": cells_global * K / (te * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d, world) / K),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h, world) / K),
+               "ms_total": te, "what": "pinned H2D of u0 and P, init (K0), K protected sweeps, "
+                                       "D2H of the field + stats; bytes are job totals / K"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(p, a.cpu_layers)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": round(tA / K, 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if p.dtype == "f32" else "f64",
+            "data": "synthetic (seeded splitmix64; Rodinia HotSpot3D inputs not available)",
+            "config": {"workload": f"{a.config}: HotSpot3D 7-point {p.nx}x{p.ny}x{p.nz} "
+                                   f"{p.dtype}, online ABFT, {K} sweeps, "
+                                   f"{len(faults)} scheduled bit-flips",
+                       "nx": p.nx, "ny": p.ny, "nz": p.nz, "z_per_gpu": zc,
+                       "parallelism": f"z-slab x{world} (NCCL halo)" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (4 GiB per array); no flush",
+                       "k1_grid": list(prof["grid"]), "k1_threads": prof["threads"],
+                       "k1_smem": prof["smem"], "k1_layers_per_cta": prof["zchunk"]},
+            "abft_overhead_pct": round((tB / tC - 1.0) * 100.0, 3),
+            "abft_overhead_with_flips_pct": round((tA / tC - 1.0) * 100.0, 3),
+            "unprotected_gcells": round(cells_global * K / (tC * 1e-3) / 1e9, 3),
+            "error_free_protected_gcells": round(cells_global * K / (tB * 1e-3) / 1e9, 3),
+            "hbm_roofline_frac_step": round(value * 1e9 * bytes_cell / (peak * 1e9) / world, 4),
+            "roofline": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(k1_gbs / peak, 4), "traffic": traffic,
+                         "kernel": "k1_sweep<float,HOTSPOT7,CHK> (protected)",
+                         "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "algorithmic_bytes_per_launch": bytes_cell * cells_local,
+                         "k1_ms": round(k1_ms, 5), "k1_unprotected_ms": round(k1_ms_unprot, 5),
+                         "k2_ms": round(k2_ms, 5)},
+            "detections": rA["stats"], "status": rA["status"],
+            "gpu_launches": int(launches),
+            "clocks": ck,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# -------------------------------------------------------------- CPU oracle
+def _oracle_sample(p, layers, sweeps):
+    """The oracle as it stands on a z-sample of the workload (same generator)."""
+    from oracle import oracle as O
+    sub = p.replace(nz=layers)
+    u0 = field_u0(sub).numpy()
+    P = field_power(sub)
+    op = O.OProblem(sub, [P.numpy()] if P is not None else [])
+    t0 = time.perf_counter()
+    O.run(op, u0, sweeps, [])
+    dt = time.perf_counter() - t0
+    return sub.cells * sweeps, dt
+
+
+def cpu_baseline(p, layers=0):
+    sweeps = 2
+    if layers <= 0:   # calibrate to ~15 s of CPU work
+        n, dt = _oracle_sample(p, 2, 1)
+        rate = n / dt
+        layers = int(max(2, min(p.nz, 15.0 * rate / (p.nx * p.ny * sweeps))))
+    n, dt = _oracle_sample(p, layers, sweeps)
+    return {"value": round(n / dt / 1e9, 6), "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "oracle",
+            "sample": f"{p.nx}x{p.ny}x{layers} layers of {p.name}, {sweeps} online sweeps, "
+                      f"{dt:.1f} s wall (C oracle, OpenMP over layers)"}
+
+
+def run_reference(a):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    p = make_problem(a.config)
+    layers = a.cpu_layers if a.cpu_layers > 0 else 4
+    from oracle import oracle as O
+    sub = p.replace(nz=layers)
+    u0 = field_u0(sub).numpy()
+    P = field_power(sub)
+    op = O.OProblem(sub, [P.numpy()] if P is not None else [])
+    for _ in range(a.warmup):
+        O.run(op, u0, 1, [])
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        O.run(op, u0, 1, [])
+    dt = time.perf_counter() - t0
+    v = sub.cells * a.steps / dt / 1e9
+    sample = (f"each step: one online protected sweep of {p.nx}x{p.ny}x{layers} layers of "
+              f"{p.name} (C oracle as it stands, incl. its per-call checksum init)")
+    line = {"metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt / a.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": p.dtype,
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{p.name} (sampled, see cpu_baseline.sample)"},
+            "cpu_baseline": {"value": round(v, 6), "unit": UNIT,
+                             "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

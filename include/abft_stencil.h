@@ -1,0 +1,240 @@
+/*
+ * abft_stencil.h -- C-ABI of the B200-native ABFT-protected stencil library
+ * (libabft_stencil.so, built from paper_1909_00709_b200/csrc/).
+ *
+ * The method is Cavelan & Ciorba, "Algorithm-Based Fault Tolerance for
+ * Parallel Stencil Computations" (arXiv 1909.00709); passages are cited as
+ * PAPER.md line numbers (P:<line>) with their section / equation / listing.
+ *
+ * One protected sweep s (s = 1, 2, ...) is, in the paper's order (fig.abft
+ * caption):
+ *   (1) u^s = C + sum_S w u^{s-1}                       Eq. 1
+ *       and the actual checksums a^s_x = sum_y u^s,     Eqs. 2-3
+ *       b^s_y = sum_x u^s of every z-layer, in the same pass (fig.sweep)
+ *   (2) the predicted checksums a', b' from a^{s-1}, b^{s-1} and the
+ *       boundary terms alpha, beta                      Theorem 1
+ *   (3) compare |a'/a - 1| > epsilon                    fig.detect
+ *   (4) locate the corrupted cell as the intersection of the flagged
+ *       row and column
+ *   (5) online: correct it and repair the checksums     Eq. 8, fig.correction
+ *       offline: compare once per window of `delta` sweeps and roll back to
+ *       the window's checkpoint on mismatch             Section IV
+ *
+ * Layout.  A field is u[z][y][x], x contiguous, dtype float (ABFT_F32) or
+ * double (ABFT_F64).  The domain is nx * ny * nz_global; this process owns
+ * the z-slab [z_begin, z_begin + z_count).  Checksums are fp64 per z-layer:
+ * A[z][x] = sum_y u (the paper's a, length nx) and B[z][y] = sum_x u (b,
+ * length ny).  Coordinates in faults and records are GLOBAL.
+ *
+ * Ownership.  The caller owns every device buffer (field buffers, aux
+ * workspace, source fields) and the CUDA stream, and keeps them alive until
+ * abft_stencil_destroy.  The library owns only the opaque handle and, when
+ * nranks > 1, its NCCL communicator.  It never allocates device memory.
+ * One handle per rank and stream; handles are not thread-safe.
+ *
+ * Errors.  Every function returns an int status: 0 = ABFT_OK, negative =
+ * hard error (nothing was launched or the handle is unusable for ECUDA),
+ * positive = resilience outcome.  abft_strerror() names a status.
+ */
+#ifndef ABFT_STENCIL_H
+#define ABFT_STENCIL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+#define ABFT_OK 0
+#define ABFT_DETECTED_UNCORRECTABLE 1 /* a flag that was not corrected (unlocated or >1 per vector) */
+#define ABFT_PERSISTENT_ERROR 3       /* offline: window still dirty after its rollback */
+#define ABFT_EINVAL (-1)              /* invalid configuration or argument */
+#define ABFT_ENOSPACE (-2)            /* a buffer is smaller than abft_stencil_workspace_size says */
+#define ABFT_ECUDA (-3)               /* CUDA runtime / driver error */
+#define ABFT_ENCCL (-4)               /* NCCL error (nranks > 1) */
+#define ABFT_EUNSUPPORTED (-5)        /* valid per the paper but not implemented on this path */
+
+/* ---- enums ---------------------------------------------------------------- */
+typedef enum { ABFT_F32 = 0, ABFT_F64 = 1 } abft_dtype;
+/* Boundary condition of Eq. 1 at the domain edge ("bounce-back" =
+ * clamp/replicate; P:407-415 periodic, zero and constant ghosts). */
+typedef enum {
+  ABFT_BC_CLAMP = 0,
+  ABFT_BC_PERIODIC = 1,
+  ABFT_BC_ZERO = 2,
+  ABFT_BC_CONSTANT = 3
+} abft_bc;
+/* NONE = unprotected sweep (the paper's No-ABFT baseline), ONLINE =
+ * detect + correct every sweep (Section III), OFFLINE = detect every `delta`
+ * sweeps + checkpoint rollback (Section IV). */
+typedef enum { ABFT_MODE_NONE = 0, ABFT_MODE_ONLINE = 1, ABFT_MODE_OFFLINE = 2 } abft_mode;
+/* abft_record.status */
+typedef enum {
+  ABFT_REC_CORRECTED = 1,     /* located by intersection, corrected (Eq. 8)      */
+  ABFT_REC_UNLOCATED = 2,     /* only one checksum vector flagged        */
+  ABFT_REC_UNCORRECTABLE = 3, /* >= 2 flagged entries in a vector of one layer    */
+  ABFT_REC_WINDOW_DIRTY = 4,  /* offline: layer flagged at a window end   */
+  ABFT_REC_PERSISTENT = 5     /* offline: layer still flagged after the rollback  */
+} abft_record_status;
+
+/* ---- problem statement ---------------------------------------------------- */
+/* One stencil point {i, j, w} of S plus the vertical offset dk of
+ * the 3D extension.  |di|, |dj|, |dk| <= 1.  The sweep evaluates
+ * the points in array order: acc = w0*v0, then acc = fma(w_p, v_p, acc). */
+typedef struct {
+  int32_t di, dj, dk, pad;
+  double w; /* rounded to the field dtype before use */
+} abft_point;
+
+/* One term of the constant C_{x,y} of Eq. 1: coef * field[z][y][x]
+ * if field != NULL, else coef * scalar.  Terms are added after the points,
+ * in array order, as acc = fma(coef, src, acc).  `field` is a DEVICE pointer
+ * to this rank's slab, dense [z_count][ny][nx] of the field dtype, read-only.
+ * At most one term may have a field. */
+typedef struct {
+  double coef;
+  const void* field;
+  double scalar;
+} abft_source;
+
+typedef struct {
+  int64_t nx, ny;       /* layer extent, >= 1 each */
+  int64_t nz_global;    /* number of z-layers of the whole domain, >= 1 */
+  int64_t z_begin;      /* first global layer of this rank's slab */
+  int64_t z_count;      /* layers owned by this rank, >= 1 */
+  int32_t dtype;        /* abft_dtype */
+  int32_t bc;           /* abft_bc; this build implements ABFT_BC_CLAMP */
+  double bc_value;      /* ghost value for ABFT_BC_CONSTANT */
+  int32_t npoints;      /* 1 .. 27 */
+  int32_t nsources;     /* 0 .. 4 */
+  const abft_point* points;   /* host array, copied at init */
+  const abft_source* sources; /* host array, copied at init */
+  double epsilon;       /* detection threshold of fig.detect, > 0 */
+  int32_t mode;         /* abft_mode */
+  int32_t delta;        /* offline detection period, >= 1 */
+  int32_t correction_form; /* 0: Eq. 8 with (a - u) re-summed over the other cells
+                              (default); 1: literal fig.correction listing */
+  int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
+  int32_t pad;
+  const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by
+                                 all ranks (nranks > 1), else NULL */
+} abft_config;
+
+/* A scheduled single bit-flip (fault model P:783-785): at sweep `sweep`
+ * (1-based) the value of cell (z, y, x) gets bit `bit` flipped after its
+ * update and before it is stored, so the checksums see the corrupted value.
+ * Each fault fires once; a rollback re-executes without it (transient). */
+typedef struct {
+  int64_t sweep, z, y, x;
+  int32_t bit, pad;
+} abft_fault;
+
+/* One detection event of one z-layer. */
+typedef struct {
+  int64_t sweep, z, y, x; /* y / x: located (or first flagged) row / column, -1 if none */
+  double observed;        /* value before correction */
+  double corrected;       /* value written back (Eq. 8) */
+  double vx, vy;          /* the two Eq. 8 estimates from a and from b */
+  int32_t status;         /* abft_record_status */
+  int32_t nflag_a, nflag_b; /* flagged entries of a (over x) and of b (over y) */
+  int32_t pad;
+} abft_record;
+
+/* Counters since init.  sweeps: sweeps executed, including the re-executed
+ * ones after offline rollbacks; detections: (sweep, layer) events with a
+ * flag; located / corrected / unlocated / uncorrectable: online outcomes;
+ * rollbacks, windows, persistent: offline windows checked, rolled back, and
+ * still dirty after their rollback. */
+typedef struct {
+  int64_t sweeps, detections, located, corrected, unlocated, uncorrectable,
+      rollbacks, windows, persistent;
+} abft_stats;
+
+typedef struct abft_stencil abft_stencil;
+
+/* ---- API ------------------------------------------------------------------ */
+
+/* Bytes of each of the (up to three) field buffers and of the aux workspace
+ * for `cfg`.  A field buffer holds the slab plus two halo layers with a
+ * padded row pitch; aux holds three generations of A/B (with halo entries),
+ * the offline prediction vectors, the constant sums c_x/c_y (Theorem 1,
+ * P:321), the device record ring and counters.  Returns ABFT_EINVAL for an
+ * invalid cfg, ABFT_EUNSUPPORTED for a valid one this build does not run. */
+int abft_stencil_workspace_size(const abft_config* cfg, size_t* field_bytes, size_t* aux_bytes);
+
+/* Create a handle.  field_bufs: 2 device buffers (NONE / ONLINE) or 3
+ * (OFFLINE: the third holds the checkpoint, rotated without copies), each of
+ * field_bytes; aux: device buffer of aux_bytes.  u0: this rank's initial
+ * slab, dense [z_count][ny][nx] of dtype, HOST or DEVICE pointer (copied).
+ * stream: cudaStream_t to run on (NULL = default stream).  Computes the
+ * trusted initial checksums a^0, b^0 and c_x, c_y, and (nranks > 1) creates
+ * the NCCL communicator and exchanges the initial halo.  Asynchronous on
+ * `stream` except for NCCL initialisation. */
+int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* aux,
+                      const void* u0, void* stream, abft_stencil** out);
+
+/* Run n protected sweeps in the configured mode (steps (1)-(5) above).
+ * NONE / ONLINE: fully asynchronous, no host synchronisation; online
+ * detection outcomes are reported by abft_stencil_stats / _records /
+ * _status.  OFFLINE: windows of `delta` sweeps (the last one may be shorter:
+ * the call's final sweep is always checked); one host synchronisation per
+ * window to read the verdict; returns ABFT_PERSISTENT_ERROR if a window
+ * stayed dirty after its rollback. */
+int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
+
+/* Explicit-control API (ONLINE / NONE handles), the paper's listings one by
+ * one.  sweep(): one sweep with the actual checksums of the result (fig.sweep).
+ * check(): predicted checksums of the last sweep (Theorem 1, fig.interpolation)
+ * compared with the actual ones (fig.detect); returns the number of flagged
+ * entries of a and b over the slab (synchronises).  correct(): locate and
+ * correct the flags of the last check (fig.correction); *ncorrected = cells
+ * written back.  step(n) is n x (sweep, check, correct) without host syncs. */
+int abft_stencil_sweep(abft_stencil* h);
+int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b);
+int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected);
+
+/* Schedule bit-flips (test / measurement hook).  Replaces the pending list;
+ * faults outside this rank's slab are ignored by this rank. */
+int abft_stencil_set_faults(abft_stencil* h, const abft_fault* faults, int32_t n);
+
+/* Read-back.  All synchronise the handle's stream. */
+/* device pointer to u[z_begin][0][0] of the current field and its row pitch
+   in elements (layer pitch = pitch * ny) */
+int abft_stencil_field(abft_stencil* h, void** dev_ptr, int64_t* pitch);
+/* copy the current slab, dense [z_count][ny][nx], to dst (HOST or DEVICE) */
+int abft_stencil_read_field(abft_stencil* h, void* dst);
+/* copy the current actual checksums A [z_count][nx], B [z_count][ny] (HOST or DEVICE) */
+int abft_stencil_checksums(abft_stencil* h, double* A, double* B);
+int abft_stencil_stats(abft_stencil* h, abft_stats* out);
+/* copy up to cap records (in device append order) to the host array out;
+   *n = total recorded (may exceed cap; the ring keeps the first entries) */
+int abft_stencil_records(abft_stencil* h, abft_record* out, int32_t cap, int64_t* n);
+/* worst resilience status so far: ABFT_OK, _DETECTED_UNCORRECTABLE or _PERSISTENT_ERROR */
+int abft_stencil_status(abft_stencil* h);
+/* logical sweep index of the current state (rollbacks do not count twice) */
+int64_t abft_stencil_sweep_count(const abft_stencil* h);
+
+/* Kernel launches issued by this handle so far (for launch accounting). */
+int64_t abft_stencil_launch_count(const abft_stencil* h);
+
+/* Measurement hook.  enable != 0: every K1 (fused sweep + checksums) and K2
+ * (predict / compare / locate / correct) launch is bracketed by CUDA events
+ * on the handle's stream.  profile_read synchronises, returns the summed
+ * device time (ms) and launch counts of each kernel since the last read, and
+ * resets them.  Also reports the K1 launch geometry (grid x, y, z, threads
+ * per CTA, dynamic shared memory bytes, layers per CTA) when geo != NULL. */
+int abft_stencil_profile(abft_stencil* h, int32_t enable);
+int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_launches,
+                              double* k2_ms, int64_t* k2_launches, int32_t geo[6]);
+
+/* Free the handle and its NCCL communicator; never the caller's buffers. */
+int abft_stencil_destroy(abft_stencil* h);
+
+const char* abft_strerror(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABFT_STENCIL_H */

@@ -1,0 +1,863 @@
+// abft_stencil.cu -- host side of libabft_stencil.so: the C-ABI of
+// include/abft_stencil.h, workspace carving, the online / offline sweep loop,
+// the fault schedule, and the z-slab halo exchange over NCCL (NVLink).
+//
+// Everything numeric runs in the sm_100a kernels of sweep.cuh / check.cuh;
+// this file only validates, lays out memory, encodes TMA descriptors and
+// sequences launches on the caller's stream.  There is no CPU fallback: a
+// missing device or driver entry point is a hard ABFT_ECUDA.
+#include <dlfcn.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "check.cuh"
+#include "common.cuh"
+#include "launch.h"
+#include "nccl.h"
+
+using namespace abft;
+
+namespace {
+
+// ------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+};
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.ok ? &api : nullptr;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+#define NSYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+  NSYM(commInitRank, "ncclCommInitRank");
+  NSYM(commDestroy, "ncclCommDestroy");
+  NSYM(groupStart, "ncclGroupStart");
+  NSYM(groupEnd, "ncclGroupEnd");
+  NSYM(send, "ncclSend");
+  NSYM(recv, "ncclRecv");
+  NSYM(allReduce, "ncclAllReduce");
+#undef NSYM
+  api.ok = api.commInitRank && api.commDestroy && api.groupStart && api.groupEnd && api.send &&
+           api.recv && api.allReduce;
+  return api.ok ? &api : nullptr;
+}
+
+// ------------------------------------------------------- TMA descriptor encode
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool encode3d(CUtensorMap* m, int dtype, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+              uint64_t pitch_bytes, uint64_t layer_bytes, uint32_t b0, uint32_t b1) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {pitch_bytes, layer_bytes};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, dtype == ABFT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                  3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  int esz;
+  int64_t px, plane;
+  size_t field_bytes;
+  // aux offsets
+  size_t off_gA[3], off_gB[3], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_st, off_src;
+  size_t aux_bytes;
+  bool pad_src;
+};
+
+int field_source(const abft_config* c) {
+  int fs = -1;
+  for (int q = 0; q < c->nsources; ++q)
+    if (c->sources[q].field) fs = q;
+  return fs;
+}
+
+int validate(const abft_config* c) {
+  if (!c) return ABFT_EINVAL;
+  if (c->nx < 1 || c->ny < 1 || c->nz_global < 1 || c->z_count < 1 || c->z_begin < 0 ||
+      c->z_begin + c->z_count > c->nz_global)
+    return ABFT_EINVAL;
+  if (c->nx > (1LL << 30) || c->ny > (1LL << 30) || c->z_count > (1LL << 30)) return ABFT_EINVAL;
+  if (c->dtype != ABFT_F32 && c->dtype != ABFT_F64) return ABFT_EINVAL;
+  if (c->bc < 0 || c->bc > 3) return ABFT_EINVAL;
+  if (c->npoints < 1 || c->npoints > kMaxPoints || !c->points) return ABFT_EINVAL;
+  for (int q = 0; q < c->npoints; ++q) {
+    const abft_point& p = c->points[q];
+    if (p.di < -1 || p.di > 1 || p.dj < -1 || p.dj > 1 || p.dk < -1 || p.dk > 1) return ABFT_EUNSUPPORTED;
+    if (!isfinite(p.w)) return ABFT_EINVAL;
+    for (int r = 0; r < q; ++r)
+      if (c->points[r].di == p.di && c->points[r].dj == p.dj && c->points[r].dk == p.dk) return ABFT_EINVAL;
+  }
+  if (c->nsources < 0 || c->nsources > kMaxSources || (c->nsources > 0 && !c->sources)) return ABFT_EINVAL;
+  int nf = 0;
+  for (int q = 0; q < c->nsources; ++q) {
+    if (!isfinite(c->sources[q].coef) || !isfinite(c->sources[q].scalar)) return ABFT_EINVAL;
+    if (c->sources[q].field) nf++;
+  }
+  if (nf > 1) return ABFT_EUNSUPPORTED;
+  if (!(c->epsilon > 0.0) || !isfinite(c->epsilon)) return ABFT_EINVAL;
+  if (c->mode < 0 || c->mode > 2) return ABFT_EINVAL;
+  if (c->mode == ABFT_MODE_OFFLINE && c->delta < 1) return ABFT_EINVAL;
+  if (c->correction_form != 0 && c->correction_form != 1) return ABFT_EINVAL;
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
+  if (c->nranks > 1) {
+    if (!c->nccl_unique_id) return ABFT_EINVAL;
+    if ((c->rank == 0) != (c->z_begin == 0)) return ABFT_EINVAL;
+    if ((c->rank == c->nranks - 1) != (c->z_begin + c->z_count == c->nz_global)) return ABFT_EINVAL;
+  } else if (c->z_begin != 0 || c->z_count != c->nz_global) {
+    return ABFT_EINVAL;
+  }
+  if (c->bc != ABFT_BC_CLAMP) return ABFT_EUNSUPPORTED;  // periodic / zero / constant: SURVEY NEXT-2
+  return ABFT_OK;
+}
+
+Layout layout(const abft_config* c) {
+  Layout L;
+  L.esz = c->dtype == ABFT_F32 ? 4 : 8;
+  const int64_t align_elems = 128 / L.esz;  // 128-byte rows: TMA strides + coalescing
+  L.px = (c->nx + align_elems - 1) / align_elems * align_elems;
+  L.plane = L.px * c->ny;
+  L.field_bytes = align_up((size_t)L.plane * (c->z_count + 2) * L.esz, 256);
+  const size_t zc2 = (size_t)c->z_count + 2;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  for (int g = 0; g < 3; ++g) { L.off_gA[g] = take(zc2 * c->nx * 8); L.off_gB[g] = take(zc2 * c->ny * 8); }
+  for (int g = 0; g < 2; ++g) { L.off_PA[g] = take(zc2 * c->nx * 8); L.off_PB[g] = take(zc2 * c->ny * 8); }
+  L.off_cA = take((size_t)c->z_count * c->nx * 8);
+  L.off_cB = take((size_t)c->z_count * c->ny * 8);
+  L.off_summ = take((size_t)c->z_count * sizeof(LayerSummary));
+  L.off_st = take(sizeof(DevState));
+  const int fs = field_source(c);
+  L.pad_src = fs >= 0 && ((c->nx * L.esz) % 16 != 0 ||
+                          (reinterpret_cast<uintptr_t>(c->sources[fs].field) % 16) != 0);
+  L.off_src = L.pad_src ? take((size_t)L.plane * c->z_count * L.esz) : 0;
+  L.aux_bytes = o;
+  return L;
+}
+
+struct PendingFault {
+  abft_fault f;
+  bool fired;
+};
+
+}  // namespace
+
+struct abft_stencil {
+  abft_config cfg;
+  std::vector<abft_point> points;
+  std::vector<abft_source> sources;
+  Layout L;
+  int nbuf = 2;
+  char* fb[3] = {nullptr, nullptr, nullptr};
+  char* aux = nullptr;
+  double* gA[3];
+  double* gB[3];
+  double* PA[2];
+  double* PB[2];
+  double *cA, *cB;
+  LayerSummary* summ;
+  DevState* st;
+  const void* src_field = nullptr;
+  int64_t src_px = 0;
+  int field_src = -1;
+  cudaStream_t stream = nullptr;
+  CUtensorMap tm_u[3];
+  CUtensorMap tm_src;
+  int shape = SHAPE_GENERIC;
+  K1Geometry geo;
+  dim3 grid1;
+  int zchunk = 1;
+  SweepParams sp;
+  CheckParams cp;
+  int cur = 0;       // buffer holding the current field
+  int prev = 1;      // buffer holding the previous field (explicit API)
+  int gen = 0;       // checksum generation of the current state
+  int gen_prev = 0;
+  bool pending_check = false;
+  bool next_zero = true;  // generation (gen + 1) % 3 is known to be zero
+  int64_t sweeps = 0;      // logical sweep index of the current state
+  int64_t executed = 0;    // sweeps executed, incl. re-executions after rollbacks
+  int64_t launches = 0;
+  int64_t rollbacks = 0, windows = 0, persistent = 0;
+  int host_worst = 0;
+  std::vector<PendingFault> faults;
+  ncclComm_t comm = nullptr;
+  int has_lo = 0, has_hi = 0;
+  // measurement hook: event pairs around K1 / K2 launches
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_kind;  // 1 = K1, 2 = K2, per pair
+  size_t ev_used = 0;        // pairs in use
+};
+
+namespace {
+
+cudaEvent_t* prof_begin(abft_stencil* h, int kind) {
+  if (!h->prof) return nullptr;
+  if (h->ev_used * 2 + 2 > h->ev.size()) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      h->ev.push_back(e);
+    }
+    h->ev_kind.push_back(0);
+  }
+  cudaEvent_t* pair = &h->ev[h->ev_used * 2];
+  h->ev_kind[h->ev_used] = kind;
+  h->ev_used++;
+  cudaEventRecord(pair[0], h->stream);
+  return pair;
+}
+void prof_end(abft_stencil* h, cudaEvent_t* pair) {
+  if (pair) cudaEventRecord(pair[1], h->stream);
+}
+
+#define CK(x)                                              \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) {                               \
+      fprintf(stderr, "abft_stencil: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return ABFT_ECUDA;                                   \
+    }                                                      \
+  } while (0)
+
+int match_shape(const abft_config* c) {
+  auto same = [&](auto shape_tag) {
+    using S = decltype(shape_tag);
+    if (c->npoints != S::NP) return false;
+    for (int q = 0; q < S::NP; ++q)
+      if (c->points[q].di != S::off(q, 0) || c->points[q].dj != S::off(q, 1) ||
+          c->points[q].dk != S::off(q, 2))
+        return false;
+    return true;
+  };
+  if (same(Shape<SHAPE_HOTSPOT7>{})) return SHAPE_HOTSPOT7;
+  if (same(Shape<SHAPE_FIG2_5PT>{})) return SHAPE_FIG2_5PT;
+  if (same(Shape<SHAPE_BOX27>{})) return SHAPE_BOX27;
+  return SHAPE_GENERIC;
+}
+
+double rnd(int dtype, double v) { return dtype == ABFT_F32 ? (double)(float)v : v; }
+
+int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk, int64_t sweep) {
+  SweepParams p = h->sp;
+  p.out = h->fb[dst];
+  p.A = A;
+  p.B = B;
+  p.nfaults = 0;
+  // this sweep's armed faults in the slab: at most one per cell per execution
+  for (auto& pf : h->faults) {
+    if (pf.fired || pf.f.sweep != sweep) continue;
+    const int64_t zl = pf.f.z - h->cfg.z_begin;
+    if (zl < 0 || zl >= h->cfg.z_count) continue;
+    bool dup = false;
+    for (int k = 0; k < p.nfaults; ++k)
+      if (p.faults[k].z == zl && p.faults[k].y == pf.f.y && p.faults[k].x == pf.f.x) dup = true;
+    if (dup || p.nfaults == kMaxFaultsPerLaunch) continue;
+    p.faults[p.nfaults++] = LocalFault{(int)zl, (int)pf.f.y, (int)pf.f.x, pf.f.bit};
+    pf.fired = true;
+  }
+  const bool inj = p.nfaults > 0;
+  h->executed++;
+  cudaEvent_t* pe = prof_begin(h, 1);
+  cudaError_t e = h->cfg.dtype == ABFT_F32
+                      ? launch_k1_f32(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], h->tm_src, p)
+                      : launch_k1_f64(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], h->tm_src, p);
+  prof_end(h, pe);
+  h->launches++;
+  CK(e);
+  return ABFT_OK;
+}
+
+int launch_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
+                 double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
+                 int flags, int64_t sweep) {
+  CheckParams p = h->cp;
+  p.uprev = h->fb[uprev];
+  p.ucur = h->fb[ucur];
+  p.Ap = Ap; p.Bp = Bp; p.Ac = Ac; p.Bc = Bc; p.PAo = PAo; p.PBo = PBo; p.zA = zA; p.zB = zB;
+  p.flags = flags;
+  p.sweep = sweep;
+  cudaEvent_t* pe = prof_begin(h, 2);
+  cudaError_t e = launch_k2(h->cfg.dtype, (int)h->cfg.z_count, h->stream, p);
+  prof_end(h, pe);
+  h->launches++;
+  CK(e);
+  return ABFT_OK;
+}
+
+// halo exchange of the boundary layers of buffer b and of the listed vectors
+int exchange(abft_stencil* h, int b, std::initializer_list<std::pair<double*, int64_t>> vecs) {
+  if (h->cfg.nranks == 1) return ABFT_OK;
+  NcclApi* n = nccl_api();
+  if (!n) return ABFT_ENCCL;
+  const ncclDataType_t dt = h->cfg.dtype == ABFT_F32 ? ncclFloat32 : ncclFloat64;
+  const int64_t zc = h->cfg.z_count;
+  const size_t lb = (size_t)h->L.plane;
+  char* buf = h->fb[b];
+  const size_t esz = h->L.esz;
+  if (n->groupStart() != ncclSuccess) return ABFT_ENCCL;
+  if (h->has_lo) {
+    n->send(buf + 1 * lb * esz, lb, dt, h->cfg.rank - 1, h->comm, h->stream);
+    n->recv(buf + 0, lb, dt, h->cfg.rank - 1, h->comm, h->stream);
+    for (auto& v : vecs) {
+      n->send(v.first + 1 * v.second, v.second, ncclFloat64, h->cfg.rank - 1, h->comm, h->stream);
+      n->recv(v.first + 0, v.second, ncclFloat64, h->cfg.rank - 1, h->comm, h->stream);
+    }
+  }
+  if (h->has_hi) {
+    n->send(buf + zc * lb * esz, lb, dt, h->cfg.rank + 1, h->comm, h->stream);
+    n->recv(buf + (zc + 1) * lb * esz, lb, dt, h->cfg.rank + 1, h->comm, h->stream);
+    for (auto& v : vecs) {
+      n->send(v.first + zc * v.second, v.second, ncclFloat64, h->cfg.rank + 1, h->comm, h->stream);
+      n->recv(v.first + (zc + 1) * v.second, v.second, ncclFloat64, h->cfg.rank + 1, h->comm, h->stream);
+    }
+  }
+  if (n->groupEnd() != ncclSuccess) return ABFT_ENCCL;
+  return ABFT_OK;
+}
+
+int zero_gen(abft_stencil* h, int g) {
+  CK(cudaMemsetAsync(h->gA[g], 0, sizeof(double) * (h->cfg.z_count + 2) * h->cfg.nx, h->stream));
+  CK(cudaMemsetAsync(h->gB[g], 0, sizeof(double) * (h->cfg.z_count + 2) * h->cfg.ny, h->stream));
+  return ABFT_OK;
+}
+
+// one online sweep s = sweeps + 1: K1 (sweep + actual checksums) then K2
+// (predict, compare, locate, correct, clear the generation of sweep s + 1)
+int online_sweep(abft_stencil* h) {
+  const int64_t s = h->sweeps + 1;
+  const int src = h->cur, dst = 1 - h->cur;
+  const int gp = h->gen, gn = (h->gen + 1) % 3, gz = (h->gen + 2) % 3;
+  int r;
+  if (!h->next_zero && (r = zero_gen(h, gn))) return r;
+  r = launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s);
+  if (r) return r;
+  r = launch_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr, nullptr,
+                   h->gA[gz], h->gB[gz], CK_COMPARE | CK_CORRECT, s);
+  if (r) return r;
+  r = exchange(h, dst, {{h->gA[gn], h->cfg.nx}, {h->gB[gn], h->cfg.ny}});
+  if (r) return r;
+  h->prev = src;
+  h->cur = dst;
+  h->gen_prev = gp;
+  h->gen = gn;
+  h->sweeps = s;
+  h->next_zero = true;  // K2 cleared generation gz = (gn + 1) % 3
+  return ABFT_OK;
+}
+
+int none_sweep(abft_stencil* h) {
+  const int64_t s = h->sweeps + 1;
+  const int src = h->cur, dst = 1 - h->cur;
+  int r = launch_k1(h, src, dst, nullptr, nullptr, false, s);
+  if (r) return r;
+  r = exchange(h, dst, {});
+  if (r) return r;
+  h->prev = src;
+  h->cur = dst;
+  h->sweeps = s;
+  return ABFT_OK;
+}
+
+int read_dirty(abft_stencil* h, int* dirty) {
+  if (h->cfg.nranks > 1) {
+    NcclApi* n = nccl_api();
+    if (!n) return ABFT_ENCCL;
+    if (n->allReduce(&h->st->dirty, &h->st->dirty, 1, ncclInt32, ncclSum, h->comm, h->stream) != ncclSuccess)
+      return ABFT_ENCCL;
+  }
+  CK(cudaMemcpyAsync(dirty, &h->st->dirty, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return ABFT_OK;
+}
+
+// Offline ABFT (Section IV): one window of L sweeps starting from
+// the checkpoint (current buffer + its actual checksums), the prediction
+// vectors advanced once per sweep (Q17), compared at the window end; on
+// mismatch the window is recomputed from the checkpoint (rotation of three
+// field buffers: no copy), a second mismatch is a persistent error.
+int offline_window(abft_stencil* h, int L) {
+  const int ck = h->cur, ckgen = h->gen, gend = (h->gen + 1) % 3;
+  const int64_t s0 = h->sweeps;
+  int others[2], k = 0;
+  for (int b = 0; b < 3; ++b)
+    if (b != ck) others[k++] = b;
+  int last = ck;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream));
+    const double* pA = h->gA[ckgen];
+    const double* pB = h->gB[ckgen];
+    int src = ck;
+    for (int t = 1; t <= L; ++t) {
+      const int64_t s = s0 + t;
+      const int dst = (src == others[0]) ? others[1] : others[0];
+      const bool end = (t == L);
+      int r;
+      if (end) {
+        r = zero_gen(h, gend);
+        if (r) return r;
+      }
+      r = launch_k1(h, src, dst, h->gA[gend], h->gB[gend], end, s);
+      if (r) return r;
+      if (!end) {
+        r = launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1], nullptr,
+                         nullptr, CK_STORE_PRED, s);
+        if (r) return r;
+        pA = h->PA[t & 1];
+        pB = h->PB[t & 1];
+        r = exchange(h, dst, {{h->PA[t & 1], h->cfg.nx}, {h->PB[t & 1], h->cfg.ny}});
+      } else {
+        r = launch_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
+                         nullptr, CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s);
+        if (r) return r;
+        r = exchange(h, dst, {{h->gA[gend], h->cfg.nx}, {h->gB[gend], h->cfg.ny}});
+      }
+      if (r) return r;
+      h->sweeps = s;
+      src = dst;
+    }
+    last = src;
+    h->windows++;
+    int dirty = 0;
+    int r = read_dirty(h, &dirty);
+    if (r) return r;
+    if (!dirty) break;
+    if (attempt == 0) {
+      h->rollbacks++;  // rollback to the checkpoint, recompute
+      h->sweeps = s0;
+    } else {
+      h->persistent++;
+      h->host_worst = 3;
+    }
+  }
+  h->prev = ck;
+  h->cur = last;
+  h->gen_prev = ckgen;
+  h->gen = gend;
+  h->next_zero = false;
+  return h->host_worst == 3 ? ABFT_PERSISTENT_ERROR : ABFT_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* abft_strerror(int s) {
+  switch (s) {
+    case ABFT_OK: return "ok";
+    case ABFT_DETECTED_UNCORRECTABLE: return "detected, not corrected";
+    case ABFT_PERSISTENT_ERROR: return "persistent error after rollback";
+    case ABFT_EINVAL: return "invalid argument";
+    case ABFT_ENOSPACE: return "workspace too small";
+    case ABFT_ECUDA: return "CUDA error";
+    case ABFT_ENCCL: return "NCCL error";
+    case ABFT_EUNSUPPORTED: return "unsupported by this build";
+    default: return "unknown status";
+  }
+}
+
+int abft_stencil_workspace_size(const abft_config* cfg, size_t* field_bytes, size_t* aux_bytes) {
+  int v = validate(cfg);
+  if (v) return v;
+  Layout L = layout(cfg);
+  if (field_bytes) *field_bytes = L.field_bytes;
+  if (aux_bytes) *aux_bytes = L.aux_bytes;
+  return ABFT_OK;
+}
+
+int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* aux, const void* u0,
+                      void* stream, abft_stencil** out) {
+  if (!out || !field_bufs || !aux || !u0) return ABFT_EINVAL;
+  *out = nullptr;
+  int v = validate(cfg);
+  if (v) return v;
+  abft_stencil* h = new abft_stencil();
+  h->cfg = *cfg;
+  h->points.assign(cfg->points, cfg->points + cfg->npoints);
+  h->sources.assign(cfg->sources, cfg->sources + cfg->nsources);
+  h->cfg.points = h->points.data();
+  h->cfg.sources = h->sources.data();
+  h->L = layout(cfg);
+  h->nbuf = cfg->mode == ABFT_MODE_OFFLINE ? 3 : 2;
+  for (int b = 0; b < h->nbuf; ++b) {
+    if (!field_bufs[b]) { delete h; return ABFT_EINVAL; }
+    h->fb[b] = static_cast<char*>(field_bufs[b]);
+  }
+  h->aux = static_cast<char*>(aux);
+  h->stream = static_cast<cudaStream_t>(stream);
+  const Layout& L = h->L;
+  for (int g = 0; g < 3; ++g) {
+    h->gA[g] = reinterpret_cast<double*>(h->aux + L.off_gA[g]);
+    h->gB[g] = reinterpret_cast<double*>(h->aux + L.off_gB[g]);
+  }
+  for (int g = 0; g < 2; ++g) {
+    h->PA[g] = reinterpret_cast<double*>(h->aux + L.off_PA[g]);
+    h->PB[g] = reinterpret_cast<double*>(h->aux + L.off_PB[g]);
+  }
+  h->cA = reinterpret_cast<double*>(h->aux + L.off_cA);
+  h->cB = reinterpret_cast<double*>(h->aux + L.off_cB);
+  h->summ = reinterpret_cast<LayerSummary*>(h->aux + L.off_summ);
+  h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
+  h->has_lo = cfg->rank > 0;
+  h->has_hi = cfg->rank < cfg->nranks - 1;
+  const int64_t nx = cfg->nx, ny = cfg->ny, zc = cfg->z_count;
+  const int esz = L.esz;
+  auto fail = [&](int code) { delete h; return code; };
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(ABFT_ECUDA);
+  if (!encode_fn()) return fail(ABFT_ECUDA);
+
+  // field: u0 (host or device, dense) -> buffer 0 layers 1..zc (padded pitch)
+  if (cudaMemsetAsync(h->fb[0], 0, L.field_bytes, h->stream) != cudaSuccess) return fail(ABFT_ECUDA);
+  if (cudaMemcpy2DAsync(h->fb[0] + (size_t)L.plane * esz, L.px * esz, u0, nx * esz, nx * esz, ny * zc,
+                        cudaMemcpyDefault, h->stream) != cudaSuccess)
+    return fail(ABFT_ECUDA);
+  for (int b = 1; b < h->nbuf; ++b)
+    if (cudaMemsetAsync(h->fb[b], 0, L.field_bytes, h->stream) != cudaSuccess) return fail(ABFT_ECUDA);
+  if (cudaMemsetAsync(h->aux, 0, L.aux_bytes, h->stream) != cudaSuccess) return fail(ABFT_ECUDA);
+
+  // source field (HotSpot power): used in place when TMA-legal, else a padded copy
+  h->field_src = field_source(cfg);
+  if (h->field_src >= 0) {
+    const void* f = cfg->sources[h->field_src].field;
+    if (L.pad_src) {
+      char* dstp = h->aux + L.off_src;
+      if (cudaMemcpy2DAsync(dstp, L.px * esz, f, nx * esz, nx * esz, ny * zc, cudaMemcpyDefault,
+                            h->stream) != cudaSuccess)
+        return fail(ABFT_ECUDA);
+      h->src_field = dstp;
+      h->src_px = L.px;
+    } else {
+      h->src_field = f;
+      h->src_px = nx;
+    }
+  }
+
+  // TMA descriptors
+  h->geo = k1_geometry(cfg->dtype);
+  const int HV = 16 / esz;
+  for (int b = 0; b < h->nbuf; ++b)
+    if (!encode3d(&h->tm_u[b], cfg->dtype, h->fb[b], nx, ny, zc + 2, L.px * esz, L.plane * esz,
+                  h->geo.tile_x + 2 * HV, h->geo.tile_y + 2))
+      return fail(ABFT_ECUDA);
+  memset(&h->tm_src, 0, sizeof(h->tm_src));
+  if (h->field_src >= 0 &&
+      !encode3d(&h->tm_src, cfg->dtype, const_cast<void*>(h->src_field), nx, ny, zc, h->src_px * esz,
+                h->src_px * ny * esz, h->geo.tile_x, h->geo.tile_y))
+    return fail(ABFT_ECUDA);
+
+  // launch geometry: z-chunks so the grid is >= ~8 waves of resident CTAs
+  h->shape = match_shape(cfg);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles_x = (int)((nx + h->geo.tile_x - 1) / h->geo.tile_x);
+  const int tiles_y = (int)((ny + h->geo.tile_y - 1) / h->geo.tile_y);
+  const int64_t tiles = (int64_t)tiles_x * tiles_y;
+  const int per_sm = std::max(1, (228 * 1024) / (h->geo.smem + 1024));
+  const int64_t target = (int64_t)8 * nsm * per_sm;
+  int64_t nch = std::max<int64_t>(1, std::min<int64_t>(zc, (target + tiles - 1) / tiles));
+  h->zchunk = (int)((zc + nch - 1) / nch);
+  if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
+  h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
+
+  // parameter blocks (weights and coefficients rounded to the dtype)
+  SweepParams& sp = h->sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.nx = (int)nx; sp.ny = (int)ny; sp.zc = (int)zc; sp.zchunk = h->zchunk;
+  sp.px = L.px; sp.plane = L.plane; sp.has_lo = h->has_lo; sp.has_hi = h->has_hi;
+  sp.npoints = cfg->npoints; sp.nsources = cfg->nsources; sp.field_src = h->field_src;
+  for (int q = 0; q < cfg->npoints; ++q) {
+    sp.di[q] = cfg->points[q].di; sp.dj[q] = cfg->points[q].dj; sp.dk[q] = cfg->points[q].dk;
+    sp.w[q] = rnd(cfg->dtype, cfg->points[q].w);
+  }
+  for (int q = 0; q < cfg->nsources; ++q) {
+    sp.coef[q] = rnd(cfg->dtype, cfg->sources[q].coef);
+    sp.scalar[q] = rnd(cfg->dtype, cfg->sources[q].scalar);
+  }
+  CheckParams& cp = h->cp;
+  memset(&cp, 0, sizeof(cp));
+  cp.nx = (int)nx; cp.ny = (int)ny; cp.zc = (int)zc; cp.px = L.px; cp.plane = L.plane;
+  cp.has_lo = h->has_lo; cp.has_hi = h->has_hi;
+  cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st;
+  cp.npoints = cfg->npoints;
+  for (int q = 0; q < cfg->npoints; ++q) {
+    cp.di[q] = sp.di[q]; cp.dj[q] = sp.dj[q]; cp.dk[q] = sp.dk[q]; cp.w[q] = sp.w[q];
+  }
+  cp.eps = cfg->epsilon;
+  cp.form = cfg->correction_form;
+  cp.z_begin = cfg->z_begin;
+
+  // K0: trusted a^0, b^0 of u0 and the pre-computed c_x, c_y
+  if (launch_k0_field(cfg->dtype, h->fb[0], L.px, L.plane, (int)nx, (int)ny, (int)zc, h->gA[0], h->gB[0],
+                      1, h->stream) != cudaSuccess)
+    return fail(ABFT_ECUDA);
+  if (launch_k0_const(cfg->dtype, h->src_field, h->src_px, (int)nx, (int)ny, (int)zc, cfg->nsources,
+                      h->field_src, sp.coef, sp.scalar, h->cA, h->cB, h->stream) != cudaSuccess)
+    return fail(ABFT_ECUDA);
+  h->launches += 4;
+
+  // multi-GPU: NCCL communicator over NVLink, initial halo
+  if (cfg->nranks > 1) {
+    NcclApi* n = nccl_api();
+    if (!n) return fail(ABFT_ENCCL);
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    if (n->commInitRank(&h->comm, cfg->nranks, id, cfg->rank) != ncclSuccess) return fail(ABFT_ENCCL);
+    int r = exchange(h, 0, {{h->gA[0], nx}, {h->gB[0], ny}});
+    if (r) { n->commDestroy(h->comm); return fail(r); }
+  }
+  *out = h;
+  return ABFT_OK;
+}
+
+int abft_stencil_step(abft_stencil* h, int32_t n) {
+  if (!h || n < 0) return ABFT_EINVAL;
+  h->pending_check = false;
+  if (h->cfg.mode == ABFT_MODE_OFFLINE) {
+    int worst = ABFT_OK;
+    while (n > 0) {
+      const int L = std::min<int>(n, h->cfg.delta);
+      int r = offline_window(h, L);
+      if (r < 0) return r;
+      worst = std::max(worst, r);
+      n -= L;
+    }
+    return worst;
+  }
+  for (int i = 0; i < n; ++i) {
+    int r = h->cfg.mode == ABFT_MODE_ONLINE ? online_sweep(h) : none_sweep(h);
+    if (r) return r;
+  }
+  return ABFT_OK;
+}
+
+int abft_stencil_sweep(abft_stencil* h) {
+  if (!h) return ABFT_EINVAL;
+  if (h->cfg.mode == ABFT_MODE_OFFLINE) return ABFT_EINVAL;
+  if (h->cfg.mode == ABFT_MODE_NONE) return none_sweep(h);
+  const int64_t s = h->sweeps + 1;
+  const int src = h->cur, dst = 1 - h->cur;
+  const int gn = (h->gen + 1) % 3;
+  int r = zero_gen(h, gn);
+  if (r) return r;
+  r = launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s);
+  if (r) return r;
+  r = exchange(h, dst, {{h->gA[gn], h->cfg.nx}, {h->gB[gn], h->cfg.ny}});
+  if (r) return r;
+  h->prev = src;
+  h->cur = dst;
+  h->gen_prev = h->gen;
+  h->gen = gn;
+  h->sweeps = s;
+  h->pending_check = true;
+  h->next_zero = false;
+  return ABFT_OK;
+}
+
+int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b) {
+  if (!h || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  CK(cudaMemsetAsync(&h->st->flag_a, 0, 2 * sizeof(long long), h->stream));
+  int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
+                       h->gB[h->gen], nullptr, nullptr, nullptr, nullptr, CK_COMPARE | CK_SUMMARY,
+                       h->sweeps);
+  if (r) return r;
+  long long f[2];
+  CK(cudaMemcpyAsync(f, &h->st->flag_a, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (nflag_a) *nflag_a = f[0];
+  if (nflag_b) *nflag_b = f[1];
+  return ABFT_OK;
+}
+
+int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected) {
+  if (!h || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  CK(cudaMemsetAsync(&h->st->ncorr, 0, sizeof(long long), h->stream));
+  int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
+                       h->gB[h->gen], nullptr, nullptr, nullptr, nullptr, CK_FROM_SUMMARY | CK_CORRECT,
+                       h->sweeps);
+  if (r) return r;
+  r = exchange(h, h->cur, {{h->gA[h->gen], h->cfg.nx}, {h->gB[h->gen], h->cfg.ny}});
+  if (r) return r;
+  long long c = 0;
+  CK(cudaMemcpyAsync(&c, &h->st->ncorr, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (ncorrected) *ncorrected = c;
+  h->pending_check = false;
+  return ABFT_OK;
+}
+
+int abft_stencil_set_faults(abft_stencil* h, const abft_fault* f, int32_t n) {
+  if (!h || n < 0 || (n > 0 && !f)) return ABFT_EINVAL;
+  h->faults.clear();
+  for (int i = 0; i < n; ++i) {
+    const abft_fault& a = f[i];
+    if (a.z < 0 || a.z >= h->cfg.nz_global || a.y < 0 || a.y >= h->cfg.ny || a.x < 0 || a.x >= h->cfg.nx ||
+        a.bit < 0 || a.bit >= 8 * h->L.esz || a.sweep < 1)
+      return ABFT_EINVAL;
+    h->faults.push_back(PendingFault{a, false});
+  }
+  return ABFT_OK;
+}
+
+int abft_stencil_field(abft_stencil* h, void** dev_ptr, int64_t* pitch) {
+  if (!h || !dev_ptr) return ABFT_EINVAL;
+  CK(cudaStreamSynchronize(h->stream));
+  *dev_ptr = h->fb[h->cur] + (size_t)h->L.plane * h->L.esz;
+  if (pitch) *pitch = h->L.px;
+  return ABFT_OK;
+}
+
+int abft_stencil_read_field(abft_stencil* h, void* dst) {
+  if (!h || !dst) return ABFT_EINVAL;
+  const size_t esz = h->L.esz;
+  CK(cudaMemcpy2DAsync(dst, h->cfg.nx * esz, h->fb[h->cur] + (size_t)h->L.plane * esz, h->L.px * esz,
+                       h->cfg.nx * esz, h->cfg.ny * h->cfg.z_count, cudaMemcpyDefault, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return ABFT_OK;
+}
+
+int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
+  if (!h || !A || !B) return ABFT_EINVAL;
+  const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
+  int g = h->gen;
+  if (h->cfg.mode == ABFT_MODE_NONE) {  // no running checksums: compute them now (Eqs. 2-3)
+    g = (h->gen + 1) % 3;
+    if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,
+                        h->gA[g], h->gB[g], 1, h->stream) != cudaSuccess)
+      return ABFT_ECUDA;
+    h->launches += 2;
+  }
+  CK(cudaMemcpyAsync(A, h->gA[g] + nx, sizeof(double) * nx * zc, cudaMemcpyDefault, h->stream));
+  CK(cudaMemcpyAsync(B, h->gB[g] + ny, sizeof(double) * ny * zc, cudaMemcpyDefault, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return ABFT_OK;
+}
+
+int abft_stencil_stats(abft_stencil* h, abft_stats* o) {
+  if (!h || !o) return ABFT_EINVAL;
+  long long c[9];
+  CK(cudaMemcpyAsync(c, h->st->cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  o->sweeps = h->executed;
+  o->detections = c[ST_DETECT];
+  o->located = c[ST_LOCATED];
+  o->corrected = c[ST_CORRECTED];
+  o->unlocated = c[ST_UNLOCATED];
+  o->uncorrectable = c[ST_UNCORR];
+  o->rollbacks = h->rollbacks;
+  o->windows = h->windows;
+  o->persistent = h->persistent;
+  return ABFT_OK;
+}
+
+int abft_stencil_records(abft_stencil* h, abft_record* out, int32_t cap, int64_t* n) {
+  if (!h || cap < 0 || (cap > 0 && !out)) return ABFT_EINVAL;
+  unsigned long long nrec = 0;
+  CK(cudaMemcpyAsync(&nrec, &h->st->nrec, sizeof(nrec), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const int64_t m = std::min<int64_t>({(int64_t)nrec, (int64_t)cap, (int64_t)kRecordCap});
+  if (m > 0) {
+    CK(cudaMemcpyAsync(out, h->st->rec, sizeof(abft_record) * m, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  if (n) *n = (int64_t)nrec;
+  return ABFT_OK;
+}
+
+int abft_stencil_status(abft_stencil* h) {
+  if (!h) return ABFT_EINVAL;
+  int w = 0;
+  CK(cudaMemcpyAsync(&w, &h->st->worst, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return std::max(w, h->host_worst);
+}
+
+int64_t abft_stencil_sweep_count(const abft_stencil* h) { return h ? h->sweeps : -1; }
+int64_t abft_stencil_launch_count(const abft_stencil* h) { return h ? h->launches : -1; }
+
+int abft_stencil_profile(abft_stencil* h, int32_t enable) {
+  if (!h) return ABFT_EINVAL;
+  h->prof = enable != 0;
+  return ABFT_OK;
+}
+
+int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_n, double* k2_ms,
+                              int64_t* k2_n, int32_t geo[6]) {
+  if (!h) return ABFT_EINVAL;
+  CK(cudaStreamSynchronize(h->stream));
+  double t[3] = {0, 0, 0};
+  int64_t n[3] = {0, 0, 0};
+  for (size_t i = 0; i < h->ev_used; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]));
+    t[h->ev_kind[i]] += ms;
+    n[h->ev_kind[i]]++;
+  }
+  h->ev_used = 0;
+  if (k1_ms) *k1_ms = t[1];
+  if (k1_n) *k1_n = n[1];
+  if (k2_ms) *k2_ms = t[2];
+  if (k2_n) *k2_n = n[2];
+  if (geo) {
+    geo[0] = h->grid1.x; geo[1] = h->grid1.y; geo[2] = h->grid1.z;
+    geo[3] = h->geo.threads; geo[4] = h->geo.smem; geo[5] = h->zchunk;
+  }
+  return ABFT_OK;
+}
+
+int abft_stencil_destroy(abft_stencil* h) {
+  if (!h) return ABFT_EINVAL;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto e : h->ev) cudaEventDestroy(e);
+  if (h->comm) {
+    NcclApi* n = nccl_api();
+    if (n) n->commDestroy(h->comm);
+  }
+  delete h;
+  return ABFT_OK;
+}
+
+}  // extern "C"

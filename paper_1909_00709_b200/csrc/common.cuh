@@ -1,0 +1,209 @@
+// common.cuh -- shared device definitions of the B200 (sm_100a) ABFT stencil path.
+// PTX wrappers for mbarrier + TMA (cp.async.bulk.tensor), the stencil shapes,
+// and the parameter blocks passed from the host library to the kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "abft_stencil.h"
+
+namespace abft {
+
+constexpr int kMaxPoints = 27;   // radius-1 stencils in 3D
+constexpr int kMaxSources = 4;
+constexpr int kMaxFaultsPerLaunch = 16;
+constexpr int kRecordCap = 4096;
+
+// ------------------------------------------------------------------ shapes
+// The sweep evaluates the points of S in the caller's order (the FMA chain is
+// part of the numeric contract).  Shapes whose point ORDER is known at compile
+// time get a register-blocked kernel; any other radius-1 list runs the generic
+// kernel (runtime offsets, same arithmetic).
+enum ShapeId { SHAPE_GENERIC = 0, SHAPE_FIG2_5PT = 1, SHAPE_HOTSPOT7 = 2, SHAPE_BOX27 = 3 };
+
+template <int S> struct Shape;
+// fig.sweep: c, w(x-1), e(x+1), s(y+1), n(y-1)
+template <> struct Shape<SHAPE_FIG2_5PT> {
+  static constexpr int NP = 5;
+  __host__ __device__ static constexpr int off(int p, int a) {
+    constexpr int t[5][3] = {{0, 0, 0}, {-1, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, -1, 0}};
+    return t[p][a];
+  }
+};
+// HotSpot3D-like (BASELINE.json configs[1]): c, w, e, n(y-1), s(y+1), t(z+1), b(z-1)
+template <> struct Shape<SHAPE_HOTSPOT7> {
+  static constexpr int NP = 7;
+  __host__ __device__ static constexpr int off(int p, int a) {
+    constexpr int t[7][3] = {{0, 0, 0},  {-1, 0, 0}, {1, 0, 0}, {0, -1, 0},
+                             {0, 1, 0},  {0, 0, 1},  {0, 0, -1}};
+    return t[p][a];
+  }
+};
+// 27-point box, dk outer, dj middle, di inner, ascending (BASELINE.json configs[4])
+template <> struct Shape<SHAPE_BOX27> {
+  static constexpr int NP = 27;
+  __host__ __device__ static constexpr int off(int p, int a) {
+    return a == 0 ? (p % 3) - 1 : (a == 1 ? (p / 3) % 3 - 1 : p / 9 - 1);
+  }
+};
+
+template <int S> __host__ __device__ constexpr bool shape_needs_z() {
+  for (int p = 0; p < Shape<S>::NP; ++p)
+    if (Shape<S>::off(p, 2) != 0) return true;
+  return false;
+}
+// does plane dk need input row offset dj (relative to an output row)?
+template <int S> __host__ __device__ constexpr bool shape_uses(int dk, int dj) {
+  for (int p = 0; p < Shape<S>::NP; ++p)
+    if (Shape<S>::off(p, 2) == dk && Shape<S>::off(p, 1) == dj) return true;
+  return false;
+}
+template <int S> __host__ __device__ constexpr bool shape_uses_x_halo(int dk) {
+  for (int p = 0; p < Shape<S>::NP; ++p)
+    if (Shape<S>::off(p, 2) == dk && Shape<S>::off(p, 0) != 0) return true;
+  return false;
+}
+
+// ------------------------------------------------------------ param blocks
+struct LocalFault { int z, y, x, bit; };  // slab-local layer, row, column
+
+struct SweepParams {
+  int nx, ny, zc, zchunk;
+  int64_t px;          // row pitch of the field buffers (elements)
+  int64_t plane;       // layer pitch = px * ny
+  int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)
+  void* out;           // output field buffer (layer 0 = lower halo)
+  double* A;           // checksum generation accumulated by this sweep, [(zc+2)][nx]
+  double* B;           // [(zc+2)][ny]
+  int npoints, nsources;
+  int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
+  double w[kMaxPoints];          // already rounded to the dtype
+  double coef[kMaxSources];      // already rounded to the dtype
+  double scalar[kMaxSources];    // already rounded to the dtype
+  int field_src;                 // index of the source with a field, -1 if none
+  int nfaults;
+  LocalFault faults[kMaxFaultsPerLaunch];
+};
+
+// per-handle device state (lives in the aux workspace)
+struct DevState {
+  unsigned long long nrec;
+  long long cnt[9];        // mirrors abft_stats order
+  int worst;               // 0 / 1 / 3
+  int dirty;               // offline: flagged layers in the last window check
+  long long flag_a, flag_b;  // explicit check(): flagged entries
+  long long ncorr;           // explicit correct(): corrections
+  abft_record rec[kRecordCap];
+};
+enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCORR,
+       ST_ROLLBACKS, ST_WINDOWS, ST_PERSIST };
+
+// per-layer summary written by check() and consumed by correct()
+struct LayerSummary {
+  int na, nb, x0, y0;
+  double pa, pb;  // predicted a'_{x0}, b'_{y0}
+};
+
+enum CheckFlags {
+  CK_STORE_PRED = 1,     // write the predicted vectors (offline P, explicit check)
+  CK_COMPARE = 2,        // compare against the actual checksums
+  CK_CORRECT = 4,        // locate + correct (online)
+  CK_OFFLINE_END = 8,    // window end: records are WINDOW_DIRTY / PERSISTENT, no correction
+  CK_PERSIST = 16,       // second attempt of a window
+  CK_SUMMARY = 32,       // write LayerSummary (explicit check())
+  CK_FROM_SUMMARY = 64,  // correct() from a stored summary, no prediction
+};
+
+struct CheckParams {
+  int nx, ny, zc;
+  int64_t px, plane;
+  int has_lo, has_hi;
+  const void* uprev;   // field buffer read by the sweep (ledger for alpha / beta)
+  void* ucur;          // field buffer written by the sweep (corrected in place)
+  const double* Ap;    // predictor input a^{s-1} (or offline P^{s-1}), [(zc+2)][nx]
+  const double* Bp;
+  double* Ac;          // actual a^s, repaired by the correction
+  double* Bc;
+  double* PAo;         // predicted output (CK_STORE_PRED), [(zc+2)][nx]
+  double* PBo;
+  const double* cA;    // c_x [zc][nx]
+  const double* cB;    // c_y [zc][ny]
+  double* zA;          // generation to clear for the next sweep (or null)
+  double* zB;
+  LayerSummary* summ;  // [zc]
+  DevState* st;
+  int npoints;
+  int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
+  double w[kMaxPoints];
+  double eps;
+  int flags, form;
+  long long sweep, z_begin;
+};
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 3D tiled TMA load of one box into shared memory, completion on `bar`
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// exact-arithmetic helpers: no contraction anywhere the numeric contract matters
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+__device__ __forceinline__ float flip_bit(float v, int bit) {
+  return __uint_as_float(__float_as_uint(v) ^ (1u << bit));
+}
+__device__ __forceinline__ double flip_bit(double v, int bit) {
+  return __longlong_as_double(__double_as_longlong(v) ^ (1ll << bit));
+}
+
+// buffer layer index of slab-local layer q in [-1, zc] (layer 0 = lower halo):
+// interior q -> q + 1; beyond a neighbour -> its halo layer; beyond the global
+// domain edge -> clamp (P:289-292 bounce-back extended to z).
+__host__ __device__ __forceinline__ int zmap(int q, int zc, int has_lo, int has_hi) {
+  if (q < 0) return has_lo ? 0 : 1;
+  if (q >= zc) return has_hi ? zc + 1 : zc;
+  return q + 1;
+}
+
+}  // namespace abft

@@ -1,0 +1,42 @@
+// K2 / K0 instantiations (see check.cuh).
+#include "check.cuh"
+#include "launch.h"
+#include "sweep.cuh"
+
+namespace abft {
+
+K1Geometry k1_geometry(int dtype) {
+  if (dtype == ABFT_F32) return {Tile<float>::TX, Tile<float>::TY, Tile<float>::SMEM, Tile<float>::THREADS};
+  return {Tile<double>::TX, Tile<double>::TY, Tile<double>::SMEM, Tile<double>::THREADS};
+}
+
+cudaError_t launch_k2(int dtype, int zc, cudaStream_t s, const CheckParams& p) {
+  if (dtype == ABFT_F32) k2_check<float><<<zc, kCheckThreads, 0, s>>>(p);
+  else k2_check<double><<<zc, kCheckThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
+                            int zc, double* A, double* B, int off, cudaStream_t s) {
+  FieldVal f{u, px, plane, dtype};
+  k0_colsum<<<dim3(zc, (nx + 255) / 256), 256, 0, s>>>(f, nx, ny, A, off);
+  k0_rowsum<<<dim3(zc, (ny + 127) / 128), 128, 0, s>>>(f, nx, ny, B, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, int ny, int zc,
+                            int nsources, int field_src, const double* coef, const double* scalar,
+                            double* cA, double* cB, cudaStream_t s) {
+  ConstVal f;
+  f.field = field; f.fpx = fpx; f.fplane = fpx * ny; f.dtype = dtype;
+  f.nsources = nsources; f.field_src = field_src;
+  for (int q = 0; q < kMaxSources; ++q) {
+    f.coef[q] = q < nsources ? coef[q] : 0.0;
+    f.scalar[q] = q < nsources ? scalar[q] : 0.0;
+  }
+  k0_colsum<<<dim3(zc, (nx + 255) / 256), 256, 0, s>>>(f, nx, ny, cA, 0);
+  k0_rowsum<<<dim3(zc, (ny + 127) / 128), 128, 0, s>>>(f, nx, ny, cB, 0);
+  return cudaGetLastError();
+}
+
+}  // namespace abft

@@ -1,0 +1,27 @@
+// launch.h -- host-side launchers of the sm_100a kernels (one translation unit
+// per dtype for K1 so the template instantiations compile in parallel).
+#pragma once
+
+#include "common.cuh"
+
+namespace abft {
+
+struct K1Geometry {
+  int tile_x, tile_y, smem, threads;
+};
+K1Geometry k1_geometry(int dtype);
+
+cudaError_t launch_k1_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
+                          const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
+cudaError_t launch_k1_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
+                          const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
+cudaError_t launch_k2(int dtype, int zc, cudaStream_t s, const CheckParams& p);
+// K0: A[z + off][x] / B[z + off][y] sums of the field buffer `u`
+cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
+                            int zc, double* A, double* B, int off, cudaStream_t s);
+// K0: c_x / c_y of the constant term
+cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, int ny, int zc,
+                            int nsources, int field_src, const double* coef, const double* scalar,
+                            double* cA, double* cB, cudaStream_t s);
+
+}  // namespace abft

@@ -1,0 +1,174 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on
+the same seeded inputs and fault schedules.  Bar (BASELINE.json north_star,
+DESIGN.md §Parity): detected / located / corrected indices bit-exact; fp32
+field values and checksums bitwise (every decision input is computed in the
+same order or exactly); fp64 fields within 1e-12, checksums within 1e-13.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from abft_inputs import Fault, Problem, fault_schedule, field_power, field_u0, make_problem
+from tests.parity_util import (assert_field_equal, gpu_run, oracle_run, parity)
+
+pytestmark = pytest.mark.gpu
+
+
+def setup_module(module):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+# ---- BASELINE.json configs at their own size (cfg1, cfg2) ------------------
+
+def test_cfg1_online_with_its_flip():
+    g, o = parity(make_problem("cfg1"))
+    assert g["launches"] > 0
+
+
+@pytest.mark.parametrize("seed", range(1, 13))
+def test_cfg1_seeds(seed):
+    # seeds exercise benign (bits 0-12) and detectable flips
+    parity(make_problem("cfg1", seed=seed))
+
+
+def test_cfg2_full_online_10_flips():
+    g, o = parity(make_problem("cfg2"))
+    assert o["stats"]["corrected"] >= 1
+
+
+def test_cfg2_explicit_api_matches_fused_step():
+    p = make_problem("cfg2", sweeps=30, nz=4)
+    parity(p, explicit=True)
+
+
+# ---- reduced cfg3 / cfg5, ragged tiles, degenerate shapes --------------------
+
+def test_cfg3_reduced_online():
+    parity(make_problem("cfg3", nz=12, sweeps=60, nfaults=8))
+
+
+def test_cfg3_reduced_offline_rollback():
+    p = make_problem("cfg3", nz=12, sweeps=60, nfaults=8, mode=2, delta=10)
+    g, o = parity(p)
+    assert o["stats"]["rollbacks"] >= 1
+
+
+def test_offline_last_window_shorter_than_delta():
+    p = make_problem("cfg3", nx=128, ny=96, nz=5, sweeps=23, nfaults=4, mode=2, delta=10)
+    parity(p)
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(203, 77, 9), (129, 33, 3), (64, 100, 2), (5, 3, 4),
+                                      (1, 1, 1), (1, 7, 3), (9, 1, 2), (260, 1, 1)])
+def test_hotspot_ragged_and_degenerate_shapes(nx, ny, nz):
+    p = make_problem("cfg2", nx=nx, ny=ny, nz=nz, sweeps=25, nfaults=2)
+    faults = [Fault(7, nz - 1, ny - 1, nx - 1, 30), Fault(15, 0, 0, 0, 27)]
+    parity(p, faults=faults)
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 64), (70, 45), (128, 33), (1, 1)])
+def test_fig2_five_point_2d(nx, ny):
+    p = make_problem("cfg1", nx=nx, ny=ny, sweeps=20)
+    parity(p, faults=[Fault(10, 0, ny // 2, nx // 3, 29)])
+
+
+def test_cfg5_reduced_fp64_box27_offline():
+    p = make_problem("cfg5", nx=130, ny=67, nz=12, sweeps=20, nfaults=6)
+    g, o = parity(p)
+
+
+def test_cfg5_reduced_fp64_box27_online():
+    p = make_problem("cfg5", nx=66, ny=40, nz=7, sweeps=15, nfaults=5, mode=1)
+    parity(p)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_generic_stencil_random_order(dtype, seed):
+    # an arbitrary radius-1 point list in arbitrary order runs the generic kernel
+    rng = random.Random(seed)
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+    rng.shuffle(offs)
+    k = rng.randint(4, 15)
+    w = [rng.uniform(0.01, 1.0) for _ in range(k)]
+    s = sum(w)
+    pts = [(a, b, c, v / s) for (a, b, c), v in zip(offs[:k], w)]
+    p = Problem("gen", 150, 61, 6, dtype, pts, [(0.002, True, 0.0), (0.5, False, 3.0)],
+                eps=1e-5 if dtype == "f32" else 1e-10, mode=1, sweeps=12, init=(1.0, 2.0),
+                power=(0.0, 1.0))
+    faults = [Fault(3, 2, 30, 70, 30 if dtype == "f32" else 62), Fault(9, 5, 60, 149, 27)]
+    parity(p, faults=faults)
+
+
+def test_correction_literal_form_runs():
+    p = make_problem("cfg1", sweeps=12, correction_form=1)
+    g = gpu_run(p, faults=[Fault(5, 0, 10, 10, 25)])
+    o = oracle_run(p, faults=[Fault(5, 0, 10, 10, 25)])
+    assert [r["x"] for r in g["records"]] == [r["x"] for r in o["records"]]
+
+
+# ---- non-interference: protection does not change the sweep (SPEC #3) -------
+
+def test_protected_field_equals_unprotected_field():
+    p = make_problem("cfg2", nz=6, sweeps=40)
+    g1 = gpu_run(p, faults=[])
+    g0 = gpu_run(p.replace(mode=0), faults=[])
+    assert np.array_equal(g1["u"].view(np.uint32), g0["u"].view(np.uint32))
+    assert g1["stats"]["detections"] == 0
+    assert np.array_equal(g1["A"], g0["A"]) and np.array_equal(g1["B"], g0["B"])
+
+
+# ---- full-size cfg4 in the launch configuration bench.py times ---------------
+
+def test_cfg4_full_size_sampled_and_properties():
+    p = make_problem("cfg4")
+    dev = torch.device("cuda:0")
+    from paper_1909_00709_b200 import abft
+    from oracle import oracle as O
+    u0 = field_u0(p, dev)
+    P = field_power(p, dev)
+    # (a) one sweep: sampled layers against the oracle, computed layer by layer
+    st = abft.from_problem(p, u0, P, device=dev)
+    st.step(1)
+    u1 = st.read_field()
+    A1, B1 = st.checksums()
+    st.destroy()
+    for z in (0, 1, 511, 1022, 1023):
+        lo, hi = max(0, z - 1), min(p.nz - 1, z + 1)
+        sub = p.replace(nz=hi - lo + 1)
+        op = O.OProblem(sub, [P[lo:hi + 1].cpu().numpy()])
+        ref = O.sweep(op, u0[lo:hi + 1].cpu().numpy())[z - lo]
+        got = u1[z].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), z
+        Ar, Br = O.checksums(O.OProblem(sub.replace(nz=1, sources=[], power=None)), ref[None])
+        assert np.array_equal(A1[z].numpy(), Ar[0]) and np.array_equal(B1[z].numpy(), Br[0])
+    del u1
+    # (b) 200 sweeps with the cfg4 schedule: every record is a scheduled flip at
+    # the injected cell; high-bit flips are all located; the corrected run stays
+    # within the correction residual of the fault-free run.
+    faults = fault_schedule(p)
+    st = abft.from_problem(p, u0, P, device=dev)
+    st.set_faults(faults)
+    st.step(p.sweeps)
+    recs = st.records()
+    uf = st.read_field()
+    st.destroy()
+    sched = {(f.sweep, f.z): f for f in faults}
+    for r in recs:
+        f = sched[(r["sweep"], r["z"])]          # no false positive
+        if r["status"] == 1:
+            assert (r["y"], r["x"]) == (f.y, f.x), r
+        else:                                     # borderline: only one vector flagged
+            assert r["status"] == 2 and (r["y"] == f.y or r["x"] == f.x), r
+    hi = [f for f in faults if f.bit >= 21]
+    got = {(r["sweep"], r["z"]) for r in recs}
+    assert all((f.sweep, f.z) in got for f in hi)
+    st = abft.from_problem(p, u0, P, device=dev)
+    st.step(p.sweeps)
+    uc = st.read_field()
+    st.destroy()
+    rel = ((uf - uc).abs() / uc.abs()).max().item()
+    assert rel < 1e-2, rel   # undetected low-bit flips diffuse; detected ones are repaired
