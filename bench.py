@@ -338,8 +338,8 @@ def _oracle_sample(p, layers, sweeps):
 
 def cpu_baseline(p, layers=0):
     sweeps = 2
-    if layers <= 0:   # calibrate to ~15 s of CPU work
-        n, dt = _oracle_sample(p, 2, 1)
+    if layers <= 0:   # calibrate to ~15 s of CPU work (>= 2 layers per thread: OpenMP over layers)
+        n, dt = _oracle_sample(p, min(p.nz, 2 * int(os.environ["OMP_NUM_THREADS"])), 1)
         rate = n / dt
         layers = int(max(2, min(p.nz, 15.0 * rate / (p.nx * p.ny * sweeps))))
     n, dt = _oracle_sample(p, layers, sweeps)

@@ -119,7 +119,9 @@ typedef struct {
   int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
   int32_t pad;
   const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by
-                                 all ranks (nranks > 1), else NULL */
+                                 all ranks (one process per GPU, nranks > 1); NULL
+                                 for nranks == 1 or for a local group member (see
+                                 abft_stencil_group) */
 } abft_config;
 
 /* A scheduled single bit-flip (fault model P:783-785): at sweep `sweep`
@@ -183,6 +185,19 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
  * window to read the verdict; returns ABFT_PERSISTENT_ERROR if a window
  * stayed dirty after its rollback. */
 int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
+
+/* Local group: n handles created by THIS process for the n slabs of one
+ * domain (cfg.nranks = n, cfg.rank = i, cfg.nccl_unique_id = NULL, slabs
+ * contiguous in rank order), on one GPU or on several peer GPUs.  group()
+ * links them and exchanges the initial halo; their halos then move by device
+ * copies (cudaMemcpyAsync, peer copies over NVLink across GPUs) ordered with
+ * events across the handles' streams, instead of NCCL.  step_group() runs n
+ * protected sweeps of every slab in lockstep (offline: windows, verdicts and
+ * rollbacks are collective).  abft_stencil_step / _sweep / _check / _correct
+ * reject grouped handles (ABFT_EINVAL).  Destroying a member dissolves the
+ * group. */
+int abft_stencil_group(abft_stencil* const* hs, int32_t n);
+int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps);
 
 /* Explicit-control API (ONLINE / NONE handles), the paper's listings one by
  * one.  sweep(): one sweep with the actual checksums of the result (fig.sweep).

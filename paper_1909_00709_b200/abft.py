@@ -29,7 +29,7 @@ EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_ste
            "abft_stencil_checksums", "abft_stencil_stats", "abft_stencil_records",
            "abft_stencil_status", "abft_stencil_sweep_count", "abft_stencil_launch_count",
            "abft_stencil_destroy", "abft_strerror", "abft_stencil_profile",
-           "abft_stencil_profile_read")
+           "abft_stencil_profile_read", "abft_stencil_group", "abft_stencil_step_group")
 
 
 class abft_point(C.Structure):
@@ -112,6 +112,8 @@ def lib() -> C.CDLL:
         L.abft_stencil_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64),
                                                 C.POINTER(C.c_double), C.POINTER(i64),
                                                 C.POINTER(i32)]
+        L.abft_stencil_group.argtypes = [C.POINTER(vp), i32]
+        L.abft_stencil_step_group.argtypes = [C.POINTER(vp), i32, i32]
         L.abft_strerror.argtypes = [C.c_int]
         L.abft_strerror.restype = C.c_char_p
         _lib = L
@@ -309,6 +311,25 @@ class Stencil:
             self.destroy()
         except Exception:
             pass
+
+
+def _handles(stencils):
+    return (C.c_void_p * len(stencils))(*[s.h.value if isinstance(s.h, C.c_void_p) else s.h
+                                          for s in stencils])
+
+
+def group(stencils: Sequence[Stencil]) -> None:
+    """abft_stencil_group: link the slab handles of one process (rank order)."""
+    hs = _handles(stencils)
+    _ok("abft_stencil_group", lib().abft_stencil_group(hs, len(stencils)))
+    for s in stencils:
+        s._group = stencils
+
+
+def step_group(stencils: Sequence[Stencil], n: int) -> int:
+    hs = _handles(stencils)
+    return _ok("abft_stencil_step_group", lib().abft_stencil_step_group(hs, len(stencils), n),
+               allow_positive=True)
 
 
 def problem_config(p, power: Optional[torch.Tensor] = None, **kw):

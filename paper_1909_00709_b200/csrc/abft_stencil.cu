@@ -102,6 +102,7 @@ struct Layout {
   size_t field_bytes;
   // aux offsets
   size_t off_gA[3], off_gB[3], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_st, off_src;
+  size_t off_EX[3];  // x-edge ledger of each field buffer, [2][zc+2][ny] of dtype
   size_t aux_bytes;
   bool pad_src;
 };
@@ -142,7 +143,6 @@ int validate(const abft_config* c) {
   if (c->correction_form != 0 && c->correction_form != 1) return ABFT_EINVAL;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
   if (c->nranks > 1) {
-    if (!c->nccl_unique_id) return ABFT_EINVAL;
     if ((c->rank == 0) != (c->z_begin == 0)) return ABFT_EINVAL;
     if ((c->rank == c->nranks - 1) != (c->z_begin + c->z_count == c->nz_global)) return ABFT_EINVAL;
   } else if (c->z_begin != 0 || c->z_count != c->nz_global) {
@@ -168,6 +168,7 @@ Layout layout(const abft_config* c) {
   L.off_cB = take((size_t)c->z_count * c->ny * 8);
   L.off_summ = take((size_t)c->z_count * sizeof(LayerSummary));
   L.off_st = take(sizeof(DevState));
+  for (int b = 0; b < 3; ++b) L.off_EX[b] = take((size_t)2 * zc2 * c->ny * L.esz);
   const int fs = field_source(c);
   L.pad_src = fs >= 0 && ((c->nx * L.esz) % 16 != 0 ||
                           (reinterpret_cast<uintptr_t>(c->sources[fs].field) % 16) != 0);
@@ -183,6 +184,9 @@ struct PendingFault {
 
 }  // namespace
 
+struct abft_stencil;
+using Group = std::vector<abft_stencil*>;
+
 struct abft_stencil {
   abft_config cfg;
   std::vector<abft_point> points;
@@ -191,6 +195,7 @@ struct abft_stencil {
   int nbuf = 2;
   char* fb[3] = {nullptr, nullptr, nullptr};
   char* aux = nullptr;
+  char* EX[3] = {nullptr, nullptr, nullptr};
   double* gA[3];
   double* gB[3];
   double* PA[2];
@@ -216,6 +221,7 @@ struct abft_stencil {
   int gen_prev = 0;
   bool pending_check = false;
   bool next_zero = true;  // generation (gen + 1) % 3 is known to be zero
+  bool summ_dirty = false; // check() left layer summaries that correct() did not consume
   int64_t sweeps = 0;      // logical sweep index of the current state
   int64_t executed = 0;    // sweeps executed, incl. re-executions after rollbacks
   int64_t launches = 0;
@@ -224,6 +230,12 @@ struct abft_stencil {
   std::vector<PendingFault> faults;
   ncclComm_t comm = nullptr;
   int has_lo = 0, has_hi = 0;
+  // local group (several slabs in one process): neighbours and sync events
+  abft_stencil* lo_peer = nullptr;
+  abft_stencil* hi_peer = nullptr;
+  bool grouped = false;
+  std::vector<abft_stencil*> members;
+  cudaEvent_t ev_ready = nullptr, ev_pulled = nullptr;
   // measurement hook: event pairs around K1 / K2 launches
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -280,9 +292,26 @@ int match_shape(const abft_config* c) {
 
 double rnd(int dtype, double v) { return dtype == ABFT_F32 ? (double)(float)v : v; }
 
+// steps (2)-(5) parameters for one sweep (see CheckParams)
+CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
+                       double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
+                       int flags, int64_t sweep) {
+  CheckParams p = h->cp;
+  p.uprev = h->fb[uprev];
+  p.ucur = h->fb[ucur];
+  p.Ap = Ap; p.Bp = Bp; p.Ac = Ac; p.Bc = Bc; p.PAo = PAo; p.PBo = PBo; p.zA = zA; p.zB = zB;
+  p.EXp = h->EX[uprev];
+  p.EXc = h->EX[ucur];
+  p.flags = flags;
+  p.sweep = sweep;
+  return p;
+}
+
+// K1: step (1)
 int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk, int64_t sweep) {
   SweepParams p = h->sp;
   p.out = h->fb[dst];
+  p.EX = h->cfg.mode != ABFT_MODE_NONE ? h->EX[dst] : nullptr;
   p.A = A;
   p.B = B;
   p.nfaults = 0;
@@ -310,52 +339,112 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk,
   return ABFT_OK;
 }
 
-int launch_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
-                 double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
-                 int flags, int64_t sweep) {
-  CheckParams p = h->cp;
-  p.uprev = h->fb[uprev];
-  p.ucur = h->fb[ucur];
-  p.Ap = Ap; p.Bp = Bp; p.Ac = Ac; p.Bc = Bc; p.PAo = PAo; p.PBo = PBo; p.zA = zA; p.zB = zB;
-  p.flags = flags;
-  p.sweep = sweep;
+// K2: steps (2)-(5) as their own launch
+int launch_check(abft_stencil* h, const CheckParams& p) {
   cudaEvent_t* pe = prof_begin(h, 2);
-  cudaError_t e = launch_k2(h->cfg.dtype, (int)h->cfg.z_count, h->stream, p);
+  cudaError_t e = launch_k2(h->cfg.dtype, h->shape, (int)h->cfg.z_count, h->stream, p);
   prof_end(h, pe);
   h->launches++;
   CK(e);
   return ABFT_OK;
 }
 
-// halo exchange of the boundary layers of buffer b and of the listed vectors
-int exchange(abft_stencil* h, int b, std::initializer_list<std::pair<double*, int64_t>> vecs) {
-  if (h->cfg.nranks == 1) return ABFT_OK;
+int launch_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
+                 double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
+                 int flags, int64_t sweep) {
+  return launch_check(h, make_check(h, uprev, ucur, Ap, Bp, Ac, Bc, PAo, PBo, zA, zB, flags, sweep));
+}
+
+// a checked sweep: K1 (step (1)) then K2 (steps (2)-(5))
+int sweep_checked(abft_stencil* h, int src, int dst, double* A, double* B, const CheckParams& ck,
+                  int64_t sweep) {
+  int r = launch_k1(h, src, dst, A, B, true, sweep);
+  if (r) return r;
+  return launch_check(h, ck);
+}
+
+// ------------------------------------------------------------------ halos
+// What crosses a slab face after a sweep: the boundary layer of field buffer
+// `buf` plus the matching entries of one pair of per-layer vectors (a
+// checksum generation or an offline prediction slot), SURVEY §8(e).
+enum { XV_NONE = 0, XV_GEN = 1, XV_P = 2 };
+struct XSpec {
+  int buf, kind, idx;
+};
+
+void xvecs(abft_stencil* h, const XSpec& x, double** a, double** b) {
+  *a = *b = nullptr;
+  if (x.kind == XV_GEN) { *a = h->gA[x.idx]; *b = h->gB[x.idx]; }
+  if (x.kind == XV_P) { *a = h->PA[x.idx]; *b = h->PB[x.idx]; }
+}
+
+// NCCL transport (one process per GPU): send / recv to rank -+ 1 in one group
+int exchange_nccl(abft_stencil* h, const XSpec& x) {
   NcclApi* n = nccl_api();
   if (!n) return ABFT_ENCCL;
   const ncclDataType_t dt = h->cfg.dtype == ABFT_F32 ? ncclFloat32 : ncclFloat64;
   const int64_t zc = h->cfg.z_count;
-  const size_t lb = (size_t)h->L.plane;
-  char* buf = h->fb[b];
-  const size_t esz = h->L.esz;
+  const size_t lb = (size_t)h->L.plane, esz = h->L.esz;
+  char* buf = h->fb[x.buf];
+  double *va, *vb;
+  xvecs(h, x, &va, &vb);
+  const std::pair<double*, int64_t> vecs[2] = {{va, h->cfg.nx}, {vb, h->cfg.ny}};
   if (n->groupStart() != ncclSuccess) return ABFT_ENCCL;
-  if (h->has_lo) {
-    n->send(buf + 1 * lb * esz, lb, dt, h->cfg.rank - 1, h->comm, h->stream);
-    n->recv(buf + 0, lb, dt, h->cfg.rank - 1, h->comm, h->stream);
-    for (auto& v : vecs) {
-      n->send(v.first + 1 * v.second, v.second, ncclFloat64, h->cfg.rank - 1, h->comm, h->stream);
-      n->recv(v.first + 0, v.second, ncclFloat64, h->cfg.rank - 1, h->comm, h->stream);
-    }
-  }
-  if (h->has_hi) {
-    n->send(buf + zc * lb * esz, lb, dt, h->cfg.rank + 1, h->comm, h->stream);
-    n->recv(buf + (zc + 1) * lb * esz, lb, dt, h->cfg.rank + 1, h->comm, h->stream);
-    for (auto& v : vecs) {
-      n->send(v.first + zc * v.second, v.second, ncclFloat64, h->cfg.rank + 1, h->comm, h->stream);
-      n->recv(v.first + (zc + 1) * v.second, v.second, ncclFloat64, h->cfg.rank + 1, h->comm, h->stream);
+  for (int side = 0; side < 2; ++side) {
+    const bool has = side == 0 ? h->has_lo : h->has_hi;
+    if (!has) continue;
+    const int peer = h->cfg.rank + (side == 0 ? -1 : 1);
+    const int64_t send_l = side == 0 ? 1 : zc, recv_l = side == 0 ? 0 : zc + 1;
+    n->send(buf + send_l * lb * esz, lb, dt, peer, h->comm, h->stream);
+    n->recv(buf + recv_l * lb * esz, lb, dt, peer, h->comm, h->stream);
+    for (const auto& v : vecs) {
+      if (!v.first) continue;
+      n->send(v.first + send_l * v.second, v.second, ncclFloat64, peer, h->comm, h->stream);
+      n->recv(v.first + recv_l * v.second, v.second, ncclFloat64, peer, h->comm, h->stream);
     }
   }
   if (n->groupEnd() != ncclSuccess) return ABFT_ENCCL;
   return ABFT_OK;
+}
+
+// local transport (several slabs driven by one process, same or peer GPUs):
+// every handle pulls its two halo layers from its neighbours with device
+// copies, ordered by events across the handles' streams.
+int exchange_local(Group& G, const XSpec& x) {
+  for (abft_stencil* h : G) CK(cudaEventRecord(h->ev_ready, h->stream));
+  for (abft_stencil* h : G) {
+    const size_t lb = (size_t)h->L.plane * h->L.esz;
+    for (int side = 0; side < 2; ++side) {
+      abft_stencil* q = side == 0 ? h->lo_peer : h->hi_peer;
+      if (!q) continue;
+      CK(cudaStreamWaitEvent(h->stream, q->ev_ready, 0));
+      const int64_t src_l = side == 0 ? q->cfg.z_count : 1;
+      const int64_t dst_l = side == 0 ? 0 : h->cfg.z_count + 1;
+      CK(cudaMemcpyAsync(h->fb[x.buf] + dst_l * lb, q->fb[x.buf] + src_l * lb, lb, cudaMemcpyDefault,
+                         h->stream));
+      double *ha, *hb, *qa, *qb;
+      xvecs(h, x, &ha, &hb);
+      xvecs(q, x, &qa, &qb);
+      if (ha) {
+        const int64_t nx = h->cfg.nx, ny = h->cfg.ny;
+        CK(cudaMemcpyAsync(ha + dst_l * nx, qa + src_l * nx, nx * 8, cudaMemcpyDefault, h->stream));
+        CK(cudaMemcpyAsync(hb + dst_l * ny, qb + src_l * ny, ny * 8, cudaMemcpyDefault, h->stream));
+      }
+    }
+    CK(cudaEventRecord(h->ev_pulled, h->stream));
+  }
+  // a neighbour may overwrite the layers we pulled only after our copies ran
+  for (abft_stencil* h : G)
+    for (abft_stencil* q : {h->lo_peer, h->hi_peer})
+      if (q) CK(cudaStreamWaitEvent(h->stream, q->ev_pulled, 0));
+  return ABFT_OK;
+}
+
+int halo_exchange(Group& G, const XSpec& x) {
+  if (G.size() > 1) return exchange_local(G, x);
+  abft_stencil* h = G[0];
+  if (h->cfg.nranks == 1) return ABFT_OK;
+  return exchange_nccl(h, x);
 }
 
 int zero_gen(abft_stencil* h, int g) {
@@ -364,120 +453,168 @@ int zero_gen(abft_stencil* h, int g) {
   return ABFT_OK;
 }
 
-// one online sweep s = sweeps + 1: K1 (sweep + actual checksums) then K2
-// (predict, compare, locate, correct, clear the generation of sweep s + 1)
-int online_sweep(abft_stencil* h) {
-  const int64_t s = h->sweeps + 1;
-  const int src = h->cur, dst = 1 - h->cur;
-  const int gp = h->gen, gn = (h->gen + 1) % 3, gz = (h->gen + 2) % 3;
-  int r;
-  if (!h->next_zero && (r = zero_gen(h, gn))) return r;
-  r = launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s);
-  if (r) return r;
-  r = launch_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr, nullptr,
-                   h->gA[gz], h->gB[gz], CK_COMPARE | CK_CORRECT, s);
-  if (r) return r;
-  r = exchange(h, dst, {{h->gA[gn], h->cfg.nx}, {h->gB[gn], h->cfg.ny}});
-  if (r) return r;
-  h->prev = src;
-  h->cur = dst;
-  h->gen_prev = gp;
-  h->gen = gn;
-  h->sweeps = s;
-  h->next_zero = true;  // K2 cleared generation gz = (gn + 1) % 3
-  return ABFT_OK;
-}
+#define TRY(...)            \
+  do {                      \
+    int r_ = (__VA_ARGS__); \
+    if (r_) return r_;      \
+  } while (0)
 
-int none_sweep(abft_stencil* h) {
-  const int64_t s = h->sweeps + 1;
-  const int src = h->cur, dst = 1 - h->cur;
-  int r = launch_k1(h, src, dst, nullptr, nullptr, false, s);
-  if (r) return r;
-  r = exchange(h, dst, {});
-  if (r) return r;
-  h->prev = src;
-  h->cur = dst;
-  h->sweeps = s;
-  return ABFT_OK;
-}
-
-int read_dirty(abft_stencil* h, int* dirty) {
-  if (h->cfg.nranks > 1) {
-    NcclApi* n = nccl_api();
-    if (!n) return ABFT_ENCCL;
-    if (n->allReduce(&h->st->dirty, &h->st->dirty, 1, ncclInt32, ncclSum, h->comm, h->stream) != ncclSuccess)
-      return ABFT_ENCCL;
+// one online sweep s = sweeps + 1 of every slab of the group: K1 (sweep +
+// actual checksums) then K2 (predict, compare, locate, correct, clear the
+// generation of sweep s + 1), then the halo of the corrected layers
+int online_sweep(Group& G) {
+  abft_stencil* h0 = G[0];
+  const int64_t s = h0->sweeps + 1;
+  const int src = h0->cur, dst = 1 - h0->cur;
+  const int gp = h0->gen, gn = (h0->gen + 1) % 3, gz = (h0->gen + 2) % 3;
+  for (abft_stencil* h : G) {
+    if (!h->next_zero) TRY(zero_gen(h, gn));
+    TRY(sweep_checked(h, src, dst, h->gA[gn], h->gB[gn],
+                      make_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr,
+                                 nullptr, h->gA[gz], h->gB[gz], CK_COMPARE | CK_CORRECT, s),
+                      s));
   }
-  CK(cudaMemcpyAsync(dirty, &h->st->dirty, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  TRY(halo_exchange(G, XSpec{dst, XV_GEN, gn}));
+  for (abft_stencil* h : G) {
+    h->prev = src;
+    h->cur = dst;
+    h->gen_prev = gp;
+    h->gen = gn;
+    h->sweeps = s;
+    h->next_zero = true;  // K2 cleared generation gz = (gn + 1) % 3
+  }
+  return ABFT_OK;
+}
+
+int none_sweep(Group& G) {
+  abft_stencil* h0 = G[0];
+  const int64_t s = h0->sweeps + 1;
+  const int src = h0->cur, dst = 1 - h0->cur;
+  for (abft_stencil* h : G) TRY(launch_k1(h, src, dst, nullptr, nullptr, false, s));
+  TRY(halo_exchange(G, XSpec{dst, XV_NONE, 0}));
+  for (abft_stencil* h : G) {
+    h->prev = src;
+    h->cur = dst;
+    h->sweeps = s;
+  }
+  return ABFT_OK;
+}
+
+// flagged layers of the last window check, summed over every slab of the job
+int read_dirty(Group& G, int* dirty) {
+  *dirty = 0;
+  for (abft_stencil* h : G) {
+    if (G.size() == 1 && h->cfg.nranks > 1) {
+      NcclApi* n = nccl_api();
+      if (!n) return ABFT_ENCCL;
+      if (n->allReduce(&h->st->dirty, &h->st->dirty, 1, ncclInt32, ncclSum, h->comm, h->stream) !=
+          ncclSuccess)
+        return ABFT_ENCCL;
+    }
+    int d = 0;
+    CK(cudaMemcpyAsync(&d, &h->st->dirty, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    *dirty += d;
+  }
   return ABFT_OK;
 }
 
 // Offline ABFT (Section IV): one window of L sweeps starting from
 // the checkpoint (current buffer + its actual checksums), the prediction
 // vectors advanced once per sweep (Q17), compared at the window end; on
-// mismatch the window is recomputed from the checkpoint (rotation of three
-// field buffers: no copy), a second mismatch is a persistent error.
-int offline_window(abft_stencil* h, int L) {
-  const int ck = h->cur, ckgen = h->gen, gend = (h->gen + 1) % 3;
-  const int64_t s0 = h->sweeps;
+// mismatch -- anywhere in the job -- every slab recomputes the window from
+// its checkpoint (rotation of three field buffers: no copy); a second
+// mismatch is a persistent error.
+int offline_window(Group& G, int L) {
+  abft_stencil* h0 = G[0];
+  const int ck = h0->cur, ckgen = h0->gen, gend = (h0->gen + 1) % 3;
+  const int64_t s0 = h0->sweeps;
   int others[2], k = 0;
   for (int b = 0; b < 3; ++b)
     if (b != ck) others[k++] = b;
   int last = ck;
+  int worst = ABFT_OK;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream));
-    const double* pA = h->gA[ckgen];
-    const double* pB = h->gB[ckgen];
+    for (abft_stencil* h : G) CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream));
     int src = ck;
     for (int t = 1; t <= L; ++t) {
       const int64_t s = s0 + t;
       const int dst = (src == others[0]) ? others[1] : others[0];
       const bool end = (t == L);
-      int r;
-      if (end) {
-        r = zero_gen(h, gend);
-        if (r) return r;
+      // P^{t-1}: the checkpoint's actual checksums for t = 1, else slot (t-1)&1
+      for (abft_stencil* h : G) {
+        const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
+        const double* pB = t == 1 ? h->gB[ckgen] : h->PB[(t - 1) & 1];
+        if (!end) {
+          TRY(launch_k1(h, src, dst, nullptr, nullptr, false, s));
+          TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
+                           nullptr, nullptr, CK_STORE_PRED, s));
+        } else {
+          TRY(zero_gen(h, gend));
+          TRY(sweep_checked(h, src, dst, h->gA[gend], h->gB[gend],
+                            make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr,
+                                       nullptr, nullptr, nullptr,
+                                       CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s),
+                            s));
+        }
       }
-      r = launch_k1(h, src, dst, h->gA[gend], h->gB[gend], end, s);
-      if (r) return r;
-      if (!end) {
-        r = launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1], nullptr,
-                         nullptr, CK_STORE_PRED, s);
-        if (r) return r;
-        pA = h->PA[t & 1];
-        pB = h->PB[t & 1];
-        r = exchange(h, dst, {{h->PA[t & 1], h->cfg.nx}, {h->PB[t & 1], h->cfg.ny}});
-      } else {
-        r = launch_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
-                         nullptr, CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s);
-        if (r) return r;
-        r = exchange(h, dst, {{h->gA[gend], h->cfg.nx}, {h->gB[gend], h->cfg.ny}});
-      }
-      if (r) return r;
-      h->sweeps = s;
+      TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1}));
+      for (abft_stencil* h : G) h->sweeps = s;
       src = dst;
     }
     last = src;
-    h->windows++;
     int dirty = 0;
-    int r = read_dirty(h, &dirty);
-    if (r) return r;
+    TRY(read_dirty(G, &dirty));
+    for (abft_stencil* h : G) h->windows++;
     if (!dirty) break;
-    if (attempt == 0) {
-      h->rollbacks++;  // rollback to the checkpoint, recompute
-      h->sweeps = s0;
-    } else {
-      h->persistent++;
-      h->host_worst = 3;
+    for (abft_stencil* h : G) {
+      if (attempt == 0) {
+        h->rollbacks++;  // rollback to the checkpoint, recompute
+        h->sweeps = s0;
+      } else {
+        h->persistent++;
+        h->host_worst = 3;
+        worst = ABFT_PERSISTENT_ERROR;
+      }
     }
   }
-  h->prev = ck;
-  h->cur = last;
-  h->gen_prev = ckgen;
-  h->gen = gend;
-  h->next_zero = false;
-  return h->host_worst == 3 ? ABFT_PERSISTENT_ERROR : ABFT_OK;
+  for (abft_stencil* h : G) {
+    h->prev = ck;
+    h->cur = last;
+    h->gen_prev = ckgen;
+    h->gen = gend;
+    h->next_zero = false;
+  }
+  return worst;
+}
+
+int clear_summaries(abft_stencil* h) {
+  if (h->summ_dirty) {
+    CK(cudaMemsetAsync(h->summ, 0, sizeof(LayerSummary) * h->cfg.z_count, h->stream));
+    h->summ_dirty = false;
+  }
+  return ABFT_OK;
+}
+
+int step_group(Group& G, int32_t n) {
+  for (abft_stencil* h : G) {
+    h->pending_check = false;
+    TRY(clear_summaries(h));
+  }
+  const int mode = G[0]->cfg.mode;
+  if (mode == ABFT_MODE_OFFLINE) {
+    int worst = ABFT_OK;
+    while (n > 0) {
+      const int L = std::min<int>(n, G[0]->cfg.delta);
+      int r = offline_window(G, L);
+      if (r < 0) return r;
+      worst = std::max(worst, r);
+      n -= L;
+    }
+    return worst;
+  }
+  for (int i = 0; i < n; ++i) TRY(mode == ABFT_MODE_ONLINE ? online_sweep(G) : none_sweep(G));
+  return ABFT_OK;
 }
 
 }  // namespace
@@ -540,6 +677,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->cA = reinterpret_cast<double*>(h->aux + L.off_cA);
   h->cB = reinterpret_cast<double*>(h->aux + L.off_cB);
   h->summ = reinterpret_cast<LayerSummary*>(h->aux + L.off_summ);
+  for (int b = 0; b < 3; ++b) h->EX[b] = h->aux + L.off_EX[b];
   h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
   h->has_lo = cfg->rank > 0;
   h->has_hi = cfg->rank < cfg->nranks - 1;
@@ -574,6 +712,15 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
       h->src_field = f;
       h->src_px = nx;
     }
+  }
+
+  // x-edge ledger of u0 (columns 0 and nx-1 of layers 1..zc), read by the first check
+  for (int side = 0; side < 2; ++side) {
+    char* dst = h->EX[0] + ((size_t)side * (zc + 2) * ny + ny) * esz;
+    const char* src = h->fb[0] + ((size_t)L.plane + (side ? nx - 1 : 0)) * esz;
+    if (cudaMemcpy2DAsync(dst, esz, src, L.px * esz, esz, ny * zc, cudaMemcpyDeviceToDevice,
+                          h->stream) != cudaSuccess)
+      return fail(ABFT_ECUDA);
   }
 
   // TMA descriptors
@@ -612,10 +759,13 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   for (int q = 0; q < cfg->npoints; ++q) {
     sp.di[q] = cfg->points[q].di; sp.dj[q] = cfg->points[q].dj; sp.dk[q] = cfg->points[q].dk;
     sp.w[q] = rnd(cfg->dtype, cfg->points[q].w);
+    sp.wf[q] = (float)sp.w[q];
   }
   for (int q = 0; q < cfg->nsources; ++q) {
     sp.coef[q] = rnd(cfg->dtype, cfg->sources[q].coef);
     sp.scalar[q] = rnd(cfg->dtype, cfg->sources[q].scalar);
+    sp.coeff[q] = (float)sp.coef[q];
+    sp.scalarf[q] = (float)sp.scalar[q];
   }
   CheckParams& cp = h->cp;
   memset(&cp, 0, sizeof(cp));
@@ -639,54 +789,74 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
     return fail(ABFT_ECUDA);
   h->launches += 4;
 
-  // multi-GPU: NCCL communicator over NVLink, initial halo
-  if (cfg->nranks > 1) {
+  // multi-GPU: NCCL communicator over NVLink, initial halo.  Without an id the
+  // handle is a member of a local group (abft_stencil_group links them).
+  if (cfg->nranks > 1 && cfg->nccl_unique_id) {
     NcclApi* n = nccl_api();
     if (!n) return fail(ABFT_ENCCL);
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     if (n->commInitRank(&h->comm, cfg->nranks, id, cfg->rank) != ncclSuccess) return fail(ABFT_ENCCL);
-    int r = exchange(h, 0, {{h->gA[0], nx}, {h->gB[0], ny}});
+    int r = exchange_nccl(h, XSpec{0, XV_GEN, 0});
     if (r) { n->commDestroy(h->comm); return fail(r); }
   }
   *out = h;
   return ABFT_OK;
 }
 
-int abft_stencil_step(abft_stencil* h, int32_t n) {
-  if (!h || n < 0) return ABFT_EINVAL;
-  h->pending_check = false;
-  if (h->cfg.mode == ABFT_MODE_OFFLINE) {
-    int worst = ABFT_OK;
-    while (n > 0) {
-      const int L = std::min<int>(n, h->cfg.delta);
-      int r = offline_window(h, L);
-      if (r < 0) return r;
-      worst = std::max(worst, r);
-      n -= L;
-    }
-    return worst;
-  }
+int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
+  if (!hs || n < 2) return ABFT_EINVAL;
   for (int i = 0; i < n; ++i) {
-    int r = h->cfg.mode == ABFT_MODE_ONLINE ? online_sweep(h) : none_sweep(h);
-    if (r) return r;
+    abft_stencil* h = hs[i];
+    if (!h || h->grouped || h->comm || h->cfg.nranks != n || h->cfg.rank != i) return ABFT_EINVAL;
+    const abft_config &a = h->cfg, &b = hs[0]->cfg;
+    if (a.nx != b.nx || a.ny != b.ny || a.nz_global != b.nz_global || a.dtype != b.dtype ||
+        a.mode != b.mode || a.delta != b.delta || a.npoints != b.npoints)
+      return ABFT_EINVAL;
+    if (i + 1 < n && a.z_begin + a.z_count != hs[i + 1]->cfg.z_begin) return ABFT_EINVAL;
+    if (h->sweeps != 0) return ABFT_EINVAL;
   }
-  return ABFT_OK;
+  Group G(hs, hs + n);
+  for (int i = 0; i < n; ++i) {
+    abft_stencil* h = hs[i];
+    h->lo_peer = i > 0 ? hs[i - 1] : nullptr;
+    h->hi_peer = i + 1 < n ? hs[i + 1] : nullptr;
+    h->grouped = true;
+    h->members = G;
+    CK(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_pulled, cudaEventDisableTiming));
+  }
+  return exchange_local(G, XSpec{0, XV_GEN, 0});  // initial halo of u^0 and a^0, b^0
+}
+
+int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps) {
+  if (!hs || n < 1 || nsweeps < 0) return ABFT_EINVAL;
+  if (n == 1) return abft_stencil_step(hs[0], nsweeps);
+  for (int i = 0; i < n; ++i)
+    if (!hs[i] || !hs[i]->grouped || hs[i]->members.size() != (size_t)n || hs[i]->members[i] != hs[i])
+      return ABFT_EINVAL;
+  Group G(hs, hs + n);
+  return step_group(G, nsweeps);
+}
+
+int abft_stencil_step(abft_stencil* h, int32_t n) {
+  if (!h || n < 0 || h->grouped) return ABFT_EINVAL;
+  Group G{h};
+  return step_group(G, n);
 }
 
 int abft_stencil_sweep(abft_stencil* h) {
-  if (!h) return ABFT_EINVAL;
+  if (!h || h->grouped) return ABFT_EINVAL;
   if (h->cfg.mode == ABFT_MODE_OFFLINE) return ABFT_EINVAL;
-  if (h->cfg.mode == ABFT_MODE_NONE) return none_sweep(h);
+  Group G{h};
+  if (h->cfg.mode == ABFT_MODE_NONE) return none_sweep(G);
   const int64_t s = h->sweeps + 1;
   const int src = h->cur, dst = 1 - h->cur;
   const int gn = (h->gen + 1) % 3;
-  int r = zero_gen(h, gn);
-  if (r) return r;
-  r = launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s);
-  if (r) return r;
-  r = exchange(h, dst, {{h->gA[gn], h->cfg.nx}, {h->gB[gn], h->cfg.ny}});
-  if (r) return r;
+  TRY(clear_summaries(h));
+  TRY(zero_gen(h, gn));
+  TRY(launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s));
+  TRY(halo_exchange(G, XSpec{dst, XV_GEN, gn}));
   h->prev = src;
   h->cur = dst;
   h->gen_prev = h->gen;
@@ -698,12 +868,14 @@ int abft_stencil_sweep(abft_stencil* h) {
 }
 
 int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b) {
-  if (!h || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  if (!h || h->grouped || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  TRY(clear_summaries(h));
   CK(cudaMemsetAsync(&h->st->flag_a, 0, 2 * sizeof(long long), h->stream));
   int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
                        h->gB[h->gen], nullptr, nullptr, nullptr, nullptr, CK_COMPARE | CK_SUMMARY,
                        h->sweeps);
   if (r) return r;
+  h->summ_dirty = true;
   long long f[2];
   CK(cudaMemcpyAsync(f, &h->st->flag_a, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -713,14 +885,15 @@ int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b) {
 }
 
 int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected) {
-  if (!h || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  if (!h || h->grouped || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
   CK(cudaMemsetAsync(&h->st->ncorr, 0, sizeof(long long), h->stream));
   int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
                        h->gB[h->gen], nullptr, nullptr, nullptr, nullptr, CK_FROM_SUMMARY | CK_CORRECT,
                        h->sweeps);
   if (r) return r;
-  r = exchange(h, h->cur, {{h->gA[h->gen], h->cfg.nx}, {h->gB[h->gen], h->cfg.ny}});
-  if (r) return r;
+  h->summ_dirty = false;
+  Group G{h};
+  TRY(halo_exchange(G, XSpec{h->cur, XV_GEN, h->gen}));
   long long c = 0;
   CK(cudaMemcpyAsync(&c, &h->st->ncorr, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -852,6 +1025,11 @@ int abft_stencil_destroy(abft_stencil* h) {
   if (!h) return ABFT_EINVAL;
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto e : h->ev) cudaEventDestroy(e);
+  if (h->ev_ready) cudaEventDestroy(h->ev_ready);
+  if (h->ev_pulled) cudaEventDestroy(h->ev_pulled);
+  for (abft_stencil* q : h->members)   // unlink: the group is unusable once a member is gone
+    if (q != h) { q->lo_peer = q->lo_peer == h ? nullptr : q->lo_peer;
+                  q->hi_peer = q->hi_peer == h ? nullptr : q->hi_peer; q->members.clear(); }
   if (h->comm) {
     NcclApi* n = nccl_api();
     if (n) n->commDestroy(h->comm);

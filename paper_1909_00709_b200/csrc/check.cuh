@@ -44,148 +44,201 @@ __device__ __forceinline__ void bump(DevState* st, int k, long long v = 1) {
   atomicAdd(reinterpret_cast<unsigned long long*>(&st->cnt[k]), (unsigned long long)v);
 }
 
-constexpr int kCheckThreads = 512;
+constexpr int kCheckThreads = 256;
 
+// one entry of a'_x (A == true) or b'_y of layer z, Theorem 1 (Eqs. 4-5):
+//   a'_x = c_x + sum_S w (a_{zeta(z+k)}[x+i] + alpha_{x+i, j})
+//   b'_y = c_y + sum_S w (b_{zeta(z+k)}[y+j] + beta_{i, y+j})
+// points in the caller's order, fp64, separately rounded; all loads issued first.
+template <typename T, int S, bool A>
+__device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int e) {
+  constexpr bool GEN = S == SHAPE_GENERIC;
+  constexpr int NPM = GEN ? kMaxPoints : Shape<(GEN ? SHAPE_HOTSPOT7 : S)>::NP;
+  const int nx = p.nx, ny = p.ny, zc = p.zc;
+  const int np = GEN ? p.npoints : NPM;
+  const T* up = reinterpret_cast<const T*>(p.uprev);
+  const T* ex = reinterpret_cast<const T*>(p.EXp);
+  const size_t side = (size_t)(zc + 2) * ny;
+  double Sv[NPM];
+#pragma unroll
+  for (int q = 0; q < NPM; ++q) {
+    if (q >= np) break;
+    int di, dj, dk;
+    if constexpr (GEN) { di = p.di[q]; dj = p.dj[q]; dk = p.dk[q]; }
+    else { di = Shape<S>::off(q, 0); dj = Shape<S>::off(q, 1); dk = Shape<S>::off(q, 2); }
+    const int zq = zmap(z + dk, zc, p.has_lo, p.has_hi);
+    if (A) {
+      const int xr = max(0, min(e + di, nx - 1));
+      double s = p.Ap[(size_t)zq * nx + xr];
+      if (dj != 0) {   // alpha at the shifted column (Q3): ghost row minus the far edge row (clamp)
+        const T* col = up + (size_t)zq * p.plane + xr;
+        const double top = (double)col[0], bot = (double)col[(size_t)(ny - 1) * p.px];
+        s = __dadd_rn(s, dj < 0 ? __dsub_rn(top, bot) : __dsub_rn(bot, top));
+      }
+      Sv[q] = s;
+    } else {
+      const int yr = max(0, min(e + dj, ny - 1));
+      double s = p.Bp[(size_t)zq * ny + yr];
+      if (di != 0) {   // beta: the x-edge columns of u^{s-1} (ledger, or the halo layer itself)
+        double lft, rgt;
+        if (ex && zq >= 1 && zq <= zc) {
+          lft = (double)ex[(size_t)zq * ny + yr];
+          rgt = (double)ex[side + (size_t)zq * ny + yr];
+        } else {
+          const T* row = up + (size_t)zq * p.plane + (size_t)yr * p.px;
+          lft = (double)row[0];
+          rgt = (double)row[nx - 1];
+        }
+        s = __dadd_rn(s, di < 0 ? __dsub_rn(lft, rgt) : __dsub_rn(rgt, lft));
+      }
+      Sv[q] = s;
+    }
+  }
+  double acc = A ? p.cA[(size_t)z * nx + e] : p.cB[(size_t)z * ny + e];
+#pragma unroll
+  for (int q = 0; q < NPM; ++q) {
+    if (q >= np) break;
+    acc = __dadd_rn(acc, __dmul_rn(p.w[q], Sv[q]));
+  }
+  return acc;
+}
+
+// Steps (4)-(5) for layer z once its compare is complete (na / nb flagged
+// entries, x0 / y0 the first flagged index, pa / pb their predictions); run by
+// every thread of one CTA of kCheckThreads threads (block-uniform arguments).
 template <typename T>
+__device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na, int nb, int x0,
+                                             int y0, double pa, double pb, double* red) {
+  const int tid = threadIdx.x, bz = z + 1, nx = p.nx, ny = p.ny, zc = p.zc;
+  if ((na | nb) == 0) return;
+  abft_record r;
+  r.sweep = p.sweep; r.z = p.z_begin + z; r.y = y0; r.x = x0;
+  r.observed = 0.0; r.corrected = 0.0; r.vx = 0.0; r.vy = 0.0;
+  r.nflag_a = na; r.nflag_b = nb; r.pad = 0;
+  if (p.flags & CK_OFFLINE_END) {
+    if (tid == 0) {
+      r.status = (p.flags & CK_PERSIST) ? ABFT_REC_PERSISTENT : ABFT_REC_WINDOW_DIRTY;
+      push_record(p.st, r);
+      bump(p.st, ST_DETECT);
+      atomicAdd(&p.st->dirty, 1);
+    }
+    return;
+  }
+  if (!(p.flags & CK_CORRECT)) return;
+  if (na == 1 && nb == 1) {
+    // ---- locate and correct (Eq. 8, fig.correction)
+    T* lay = reinterpret_cast<T*>(p.ucur) + (size_t)bz * p.plane;
+    double sx = 0.0, sy = 0.0;
+    if (p.form == 0) {   // (a - u) as the sum of the other cells (Q11)
+      for (int y = tid; y < ny; y += kCheckThreads)
+        if (y != y0) sx += (double)lay[(size_t)y * p.px + x0];
+      for (int x = tid; x < nx; x += kCheckThreads)
+        if (x != x0) sy += (double)lay[(size_t)y0 * p.px + x];
+    }
+    sx = block_sum<kCheckThreads>(sx, red);
+    sy = block_sum<kCheckThreads>(sy, red);
+    if (tid == 0) {
+      T* cell = lay + (size_t)y0 * p.px + x0;
+      const double uo = (double)*cell;
+      double* ax = &p.Ac[(size_t)bz * nx + x0];
+      double* by = &p.Bc[(size_t)bz * ny + y0];
+      double vx, vy;
+      T cor;
+      if (p.form == 0) {
+        vx = pa - sx;
+        vy = pb - sy;
+        cor = (T)((vx + vy) / 2.0);
+        *ax = sx + (double)cor;   // exact repair (Q12)
+        *by = sy + (double)cor;
+      } else {                    // literal listing
+        vx = pa - (*ax - uo);
+        vy = pb - (*by - uo);
+        cor = (T)((vx + vy) / 2.0);
+        *ax += (double)cor - uo;
+        *by += (double)cor - uo;
+      }
+      *cell = cor;
+      if (p.EXc) {   // keep the edge ledger of u^s in step with the field
+        T* exc = reinterpret_cast<T*>(p.EXc);
+        if (x0 == 0) exc[(size_t)bz * ny + y0] = cor;
+        if (x0 == nx - 1) exc[(size_t)(zc + 2) * ny + (size_t)bz * ny + y0] = cor;
+      }
+      r.observed = uo; r.corrected = (double)cor; r.vx = vx; r.vy = vy;
+      r.status = ABFT_REC_CORRECTED;
+      push_record(p.st, r);
+      bump(p.st, ST_DETECT); bump(p.st, ST_LOCATED); bump(p.st, ST_CORRECTED);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->ncorr), 1ull);
+    }
+  } else if (tid == 0) {
+    r.status = (na == 0 || nb == 0) ? ABFT_REC_UNLOCATED : ABFT_REC_UNCORRECTABLE;
+    push_record(p.st, r);
+    bump(p.st, ST_DETECT);
+    bump(p.st, r.status == ABFT_REC_UNLOCATED ? ST_UNLOCATED : ST_UNCORR);
+    atomicMax(&p.st->worst, 1);
+  }
+}
+
+// K2.  grid (zc, ceil((nx + ny) / kCheckThreads)): every thread owns one entry
+// of a' or b' of layer blockIdx.x; the CTA that completes a layer last (per-layer
+// counter) locates, corrects and records (Eq. 8, fig.correction).
+template <typename T, int S>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
   const int z = blockIdx.x, bz = z + 1;
   const int nx = p.nx, ny = p.ny, zc = p.zc;
   const int tid = threadIdx.x;
-  __shared__ int s_na, s_nb, s_x0, s_y0;
-  __shared__ double s_pa, s_pb;
+  LayerSummary* L = &p.summ[z];
+  __shared__ int s_last;
   __shared__ double red[kCheckThreads / 32];
-  const T* up = reinterpret_cast<const T*>(p.uprev);
-  T* uc = reinterpret_cast<T*>(p.ucur);
-  if (tid == 0) {
-    s_na = 0; s_nb = 0; s_x0 = 0x7fffffff; s_y0 = 0x7fffffff; s_pa = 0.0; s_pb = 0.0;
-    if (p.flags & CK_FROM_SUMMARY) {
-      const LayerSummary L = p.summ[z];
-      s_na = L.na; s_nb = L.nb; s_x0 = L.x0; s_y0 = L.y0; s_pa = L.pa; s_pb = L.pb;
-    }
-  }
-  __syncthreads();
   if (!(p.flags & CK_FROM_SUMMARY)) {
-    // ---- a'_x, Theorem 1 (Eq. 4): c_x + sum_S w (a_{x+i} + alpha_{x+i,j})
-    for (int x = tid; x < nx; x += kCheckThreads) {
-      double pa = p.cA[(size_t)z * nx + x];
-      for (int q = 0; q < p.npoints; ++q) {
-        const int zq = zmap(z + p.dk[q], zc, p.has_lo, p.has_hi);
-        const int xr = max(0, min(x + p.di[q], nx - 1));
-        double S = p.Ap[(size_t)zq * nx + xr];
-        if (p.dj[q] != 0) {
-          const T* col = up + (size_t)zq * p.plane + xr;
-          const double top = (double)col[0], bot = (double)col[(size_t)(ny - 1) * p.px];
-          S = __dadd_rn(S, p.dj[q] < 0 ? __dsub_rn(top, bot) : __dsub_rn(bot, top));
-        }
-        pa = __dadd_rn(pa, __dmul_rn(p.w[q], S));
+    const int e = blockIdx.y * kCheckThreads + tid;
+    if (e < nx) {
+      const double pa = predict_entry<T, S, true>(p, z, e);
+      if (p.flags & CK_STORE_PRED) p.PAo[(size_t)bz * nx + e] = pa;
+      if ((p.flags & CK_COMPARE) && flag_rel(pa, p.Ac[(size_t)bz * nx + e], p.eps)) {
+        atomicAdd(&L->na, 1);
+        atomicMax(&L->xk, 0x7fffffff - e);
+        L->pa = pa;
+        __threadfence();
       }
-      if (p.flags & CK_STORE_PRED) p.PAo[(size_t)bz * nx + x] = pa;
-      if ((p.flags & CK_COMPARE) && flag_rel(pa, p.Ac[(size_t)bz * nx + x], p.eps)) {
-        atomicAdd(&s_na, 1);
-        atomicMin(&s_x0, x);
-        s_pa = pa;
-      }
-    }
-    // ---- b'_y, Theorem 1 (Eq. 5): c_y + sum_S w (b_{y+j} + beta_{i,y+j})
-    for (int y = tid; y < ny; y += kCheckThreads) {
-      double pb = p.cB[(size_t)z * ny + y];
-      for (int q = 0; q < p.npoints; ++q) {
-        const int zq = zmap(z + p.dk[q], zc, p.has_lo, p.has_hi);
-        const int yr = max(0, min(y + p.dj[q], ny - 1));
-        double S = p.Bp[(size_t)zq * ny + yr];
-        if (p.di[q] != 0) {
-          const T* row = up + (size_t)zq * p.plane + (size_t)yr * p.px;
-          const double lft = (double)row[0], rgt = (double)row[nx - 1];
-          S = __dadd_rn(S, p.di[q] < 0 ? __dsub_rn(lft, rgt) : __dsub_rn(rgt, lft));
-        }
-        pb = __dadd_rn(pb, __dmul_rn(p.w[q], S));
-      }
+      if (p.zA) p.zA[(size_t)bz * nx + e] = 0.0;   // generation of the next sweep
+    } else if (e < nx + ny) {
+      const int y = e - nx;
+      const double pb = predict_entry<T, S, false>(p, z, y);
       if (p.flags & CK_STORE_PRED) p.PBo[(size_t)bz * ny + y] = pb;
       if ((p.flags & CK_COMPARE) && flag_rel(pb, p.Bc[(size_t)bz * ny + y], p.eps)) {
-        atomicAdd(&s_nb, 1);
-        atomicMin(&s_y0, y);
-        s_pb = pb;
+        atomicAdd(&L->nb, 1);
+        atomicMax(&L->yk, 0x7fffffff - y);
+        L->pb = pb;
+        __threadfence();
       }
+      if (p.zB) p.zB[(size_t)bz * ny + y] = 0.0;
     }
-  }
-  __syncthreads();
-  const int na = s_na, nb = s_nb;
-  if (p.flags & CK_SUMMARY) {
+    if (!(p.flags & CK_COMPARE)) return;
+    __syncthreads();
     if (tid == 0) {
-      LayerSummary L;
-      L.na = na; L.nb = nb; L.x0 = na ? s_x0 : -1; L.y0 = nb ? s_y0 : -1; L.pa = s_pa; L.pb = s_pb;
-      p.summ[z] = L;
+      __threadfence();
+      s_last = atomicAdd(&L->done, 1) == (int)gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+  }
+  // ---- this CTA sees the whole layer's compare
+  const int na = *(volatile int*)&L->na, nb = *(volatile int*)&L->nb;
+  const int x0 = na ? 0x7fffffff - *(volatile int*)&L->xk : -1;
+  const int y0 = nb ? 0x7fffffff - *(volatile int*)&L->yk : -1;
+  const double pa = *(volatile double*)&L->pa, pb = *(volatile double*)&L->pb;
+  if (p.flags & CK_SUMMARY) {   // explicit check(): keep the summary for correct()
+    if (tid == 0) {
+      L->done = 0;
       if (na) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_a), (unsigned long long)na);
       if (nb) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_b), (unsigned long long)nb);
     }
-  } else if ((p.flags & (CK_COMPARE | CK_FROM_SUMMARY)) && (na | nb)) {
-    abft_record r;
-    r.sweep = p.sweep; r.z = p.z_begin + z;
-    r.y = nb ? s_y0 : -1; r.x = na ? s_x0 : -1;
-    r.observed = 0.0; r.corrected = 0.0; r.vx = 0.0; r.vy = 0.0;
-    r.nflag_a = na; r.nflag_b = nb; r.pad = 0;
-    if (p.flags & CK_OFFLINE_END) {
-      if (tid == 0) {
-        r.status = (p.flags & CK_PERSIST) ? ABFT_REC_PERSISTENT : ABFT_REC_WINDOW_DIRTY;
-        push_record(p.st, r);
-        bump(p.st, ST_DETECT);
-        atomicAdd(&p.st->dirty, 1);
-      }
-    } else if (p.flags & CK_CORRECT) {
-      if (na == 1 && nb == 1) {
-        // ---- locate and correct (Eq. 8, fig.correction)
-        const int x0 = s_x0, y0 = s_y0;
-        T* lay = uc + (size_t)bz * p.plane;
-        double sx = 0.0, sy = 0.0;
-        if (p.form == 0) {
-          for (int y = tid; y < ny; y += kCheckThreads)
-            if (y != y0) sx += (double)lay[(size_t)y * p.px + x0];
-          for (int x = tid; x < nx; x += kCheckThreads)
-            if (x != x0) sy += (double)lay[(size_t)y0 * p.px + x];
-        }
-        sx = block_sum<kCheckThreads>(sx, red);
-        sy = block_sum<kCheckThreads>(sy, red);
-        if (tid == 0) {
-          T* cell = lay + (size_t)y0 * p.px + x0;
-          const double uo = (double)*cell;
-          double* ax = &p.Ac[(size_t)bz * nx + x0];
-          double* by = &p.Bc[(size_t)bz * ny + y0];
-          double vx, vy;
-          T cor;
-          if (p.form == 0) {
-            vx = s_pa - sx;
-            vy = s_pb - sy;
-            cor = (T)((vx + vy) / 2.0);
-            *ax = sx + (double)cor;
-            *by = sy + (double)cor;
-          } else {
-            vx = s_pa - (*ax - uo);
-            vy = s_pb - (*by - uo);
-            cor = (T)((vx + vy) / 2.0);
-            *ax += (double)cor - uo;
-            *by += (double)cor - uo;
-          }
-          *cell = cor;
-          r.observed = uo; r.corrected = (double)cor; r.vx = vx; r.vy = vy;
-          r.status = ABFT_REC_CORRECTED;
-          push_record(p.st, r);
-          bump(p.st, ST_DETECT); bump(p.st, ST_LOCATED); bump(p.st, ST_CORRECTED);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->ncorr), 1ull);
-        }
-      } else if (tid == 0) {
-        r.status = (na == 0 || nb == 0) ? ABFT_REC_UNLOCATED : ABFT_REC_UNCORRECTABLE;
-        push_record(p.st, r);
-        bump(p.st, ST_DETECT);
-        bump(p.st, r.status == ABFT_REC_UNLOCATED ? ST_UNLOCATED : ST_UNCORR);
-        atomicMax(&p.st->worst, 1);
-      }
-    }
+    return;
   }
-  // clear the checksum generation the next sweep accumulates into
-  if (p.zA)
-    for (int x = tid; x < nx; x += kCheckThreads) p.zA[(size_t)bz * nx + x] = 0.0;
-  if (p.zB)
-    for (int y = tid; y < ny; y += kCheckThreads) p.zB[(size_t)bz * ny + y] = 0.0;
+  __syncthreads();
+  if (tid == 0) { L->na = 0; L->nb = 0; L->xk = 0; L->yk = 0; L->done = 0; }
+  finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
 }
 
 // ---------------------------------------------------------------- K0

@@ -69,23 +69,7 @@ template <int S> __host__ __device__ constexpr bool shape_uses_x_halo(int dk) {
 // ------------------------------------------------------------ param blocks
 struct LocalFault { int z, y, x, bit; };  // slab-local layer, row, column
 
-struct SweepParams {
-  int nx, ny, zc, zchunk;
-  int64_t px;          // row pitch of the field buffers (elements)
-  int64_t plane;       // layer pitch = px * ny
-  int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)
-  void* out;           // output field buffer (layer 0 = lower halo)
-  double* A;           // checksum generation accumulated by this sweep, [(zc+2)][nx]
-  double* B;           // [(zc+2)][ny]
-  int npoints, nsources;
-  int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
-  double w[kMaxPoints];          // already rounded to the dtype
-  double coef[kMaxSources];      // already rounded to the dtype
-  double scalar[kMaxSources];    // already rounded to the dtype
-  int field_src;                 // index of the source with a field, -1 if none
-  int nfaults;
-  LocalFault faults[kMaxFaultsPerLaunch];
-};
+
 
 // per-handle device state (lives in the aux workspace)
 struct DevState {
@@ -101,9 +85,13 @@ enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCO
        ST_ROLLBACKS, ST_WINDOWS, ST_PERSIST };
 
 // per-layer summary written by check() and consumed by correct()
+// Zero-initialised; the CTA that finishes a layer last consumes and resets it.
 struct LayerSummary {
-  int na, nb, x0, y0;
-  double pa, pb;  // predicted a'_{x0}, b'_{y0}
+  int na, nb;      // flagged entries of a (over x) and b (over y)
+  int xk, yk;      // max of (INT_MAX - index) over flagged entries: the first flagged index
+  int done;        // CTAs of this layer that finished the compare
+  int pad;
+  double pa, pb;   // predicted a'_{x0}, b'_{y0} (meaningful when na == 1 / nb == 1)
 };
 
 enum CheckFlags {
@@ -132,6 +120,8 @@ struct CheckParams {
   const double* cB;    // c_y [zc][ny]
   double* zA;          // generation to clear for the next sweep (or null)
   double* zB;
+  const void* EXp;     // edge columns x = 0 / nx-1 of uprev, [2][zc+2][ny] (interior layers)
+  void* EXc;           // edge columns of ucur (patched by a correction)
   LayerSummary* summ;  // [zc]
   DevState* st;
   int npoints;
@@ -140,6 +130,28 @@ struct CheckParams {
   double eps;
   int flags, form;
   long long sweep, z_begin;
+};
+
+struct SweepParams {
+  int nx, ny, zc, zchunk;
+  int64_t px;          // row pitch of the field buffers (elements)
+  int64_t plane;       // layer pitch = px * ny
+  int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)
+  void* out;           // output field buffer (layer 0 = lower halo)
+  double* A;           // checksum generation accumulated by this sweep, [(zc+2)][nx]
+  double* B;           // [(zc+2)][ny]
+  int npoints, nsources;
+  int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
+  double w[kMaxPoints];          // already rounded to the dtype
+  double coef[kMaxSources];      // already rounded to the dtype
+  double scalar[kMaxSources];    // already rounded to the dtype
+  float wf[kMaxPoints];          // the same values as float (fp32 fields; exact)
+  float coeff[kMaxSources];
+  float scalarf[kMaxSources];
+  int field_src;                 // index of the source with a field, -1 if none
+  void* EX;            // edge columns of the output: [2][zc+2][ny] (x = 0, x = nx-1), or null
+  int nfaults;
+  LocalFault faults[kMaxFaultsPerLaunch];
 };
 
 // ------------------------------------------------------------- PTX helpers
@@ -189,6 +201,17 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// parameter-space weights in the field dtype (no per-use conversion)
+template <typename T> __device__ __forceinline__ T pw(const SweepParams& p, int q);
+template <> __device__ __forceinline__ float pw<float>(const SweepParams& p, int q) { return p.wf[q]; }
+template <> __device__ __forceinline__ double pw<double>(const SweepParams& p, int q) { return p.w[q]; }
+template <typename T> __device__ __forceinline__ T pcoef(const SweepParams& p, int q);
+template <> __device__ __forceinline__ float pcoef<float>(const SweepParams& p, int q) { return p.coeff[q]; }
+template <> __device__ __forceinline__ double pcoef<double>(const SweepParams& p, int q) { return p.coef[q]; }
+template <typename T> __device__ __forceinline__ T pscal(const SweepParams& p, int q);
+template <> __device__ __forceinline__ float pscal<float>(const SweepParams& p, int q) { return p.scalarf[q]; }
+template <> __device__ __forceinline__ double pscal<double>(const SweepParams& p, int q) { return p.scalar[q]; }
 
 __device__ __forceinline__ float flip_bit(float v, int bit) {
   return __uint_as_float(__float_as_uint(v) ^ (1u << bit));

@@ -10,10 +10,21 @@ K1Geometry k1_geometry(int dtype) {
   return {Tile<double>::TX, Tile<double>::TY, Tile<double>::SMEM, Tile<double>::THREADS};
 }
 
-cudaError_t launch_k2(int dtype, int zc, cudaStream_t s, const CheckParams& p) {
-  if (dtype == ABFT_F32) k2_check<float><<<zc, kCheckThreads, 0, s>>>(p);
-  else k2_check<double><<<zc, kCheckThreads, 0, s>>>(p);
+template <typename T>
+static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
+  switch (shape) {
+    case SHAPE_FIG2_5PT: k2_check<T, SHAPE_FIG2_5PT><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7: k2_check<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_BOX27: k2_check<T, SHAPE_BOX27><<<g, kCheckThreads, 0, s>>>(p); break;
+    default: k2_check<T, SHAPE_GENERIC><<<g, kCheckThreads, 0, s>>>(p); break;
+  }
   return cudaGetLastError();
+}
+
+cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p) {
+  const int nblk = (p.flags & CK_FROM_SUMMARY) ? 1 : (p.nx + p.ny + kCheckThreads - 1) / kCheckThreads;
+  const dim3 g(zc, nblk);
+  return dtype == ABFT_F32 ? k2_go<float>(shape, g, s, p) : k2_go<double>(shape, g, s, p);
 }
 
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,

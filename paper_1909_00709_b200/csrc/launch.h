@@ -15,7 +15,7 @@ cudaError_t launch_k1_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t
                           const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
 cudaError_t launch_k1_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
-cudaError_t launch_k2(int dtype, int zc, cudaStream_t s, const CheckParams& p);
+cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
 // K0: A[z + off][x] / B[z + off][y] sums of the field buffer `u`
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s);

@@ -31,14 +31,20 @@ template <typename T> struct Tile {
   static constexpr int HX = TX + 2 * HV;          // staged row length
   static constexpr int WARPS = 8;
   static constexpr int THREADS = 32 * WARPS;
-  static constexpr int RY = sizeof(T) == 4 ? 4 : 2;  // output rows per thread
+#ifndef ABFT_RY_F32
+#define ABFT_RY_F32 4
+#endif
+#ifndef ABFT_NS
+#define ABFT_NS 4
+#endif
+  static constexpr int RY = sizeof(T) == 4 ? ABFT_RY_F32 : 2;  // output rows per thread
   static constexpr int TY = WARPS * RY;
   static constexpr int ROWS = TY + 2;
   static constexpr int T_BYTES = ROWS * HX * (int)sizeof(T);
   static constexpr int T_STRIDE = (T_BYTES + 127) / 128 * 128;
   static constexpr int P_BYTES = TX * TY * (int)sizeof(T);
   static constexpr int P_STRIDE = (P_BYTES + 127) / 128 * 128;
-  static constexpr int NS = 4;    // field-layer ring: z-1, z, z+1 + 1 prefetch
+  static constexpr int NS = ABFT_NS;  // field-layer ring: z-1, z, z+1 + 1 prefetch
   static constexpr int NSP = 2;   // source-layer ring
   static constexpr int PART_BYTES = WARPS * TX * 8;
   static constexpr int BAR_BYTES = 128;
@@ -91,6 +97,84 @@ template <int RY> __device__ __forceinline__ bool final_lane(int l);
 template <> __device__ __forceinline__ bool final_lane<4>(int l) { return (l & 7) == 0; }
 template <> __device__ __forceinline__ bool final_lane<2>(int l) { return (l & 15) == 0; }
 
+// fp64 row (over this thread's V columns) and column (over its RY rows)
+// partial sums of the stored values; out-of-domain cells count 0 (!FULL).
+template <typename T, bool FULL>
+__device__ __forceinline__ void partial_sums(const T (&out)[Tile<T>::RY][Tile<T>::V],
+                                             double (&rs)[Tile<T>::RY], double (&cs)[Tile<T>::V],
+                                             int gyb, int gx0, int nx, int ny) {
+  constexpr int RY = Tile<T>::RY, V = Tile<T>::V;
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double d = (double)out[r][k];
+      if (!FULL) d = (gyb + r < ny && gx0 + k < nx) ? d : 0.0;
+      rs[r] = k == 0 ? d : rs[r] + d;
+      cs[k] = r == 0 ? d : cs[k] + d;
+    }
+  }
+}
+
+// One layer of one thread: RY x V outputs of Eq. 1 from the staged layers
+// pl[0..2] (z-1, z, z+1), the canonical FMA chain in the shape's point order.
+// EDGE: the tile touches x = 0 or x = nx - 1, so out-of-domain x reads take
+// the clamped value; y is clamped through srow.
+template <typename T, int SS, bool NZ, bool EDGE>
+__device__ __forceinline__ void stencil_layer(T (&out)[Tile<T>::RY][Tile<T>::V], const T* const (&pl)[3],
+                                              const int (&srow)[Tile<T>::RY + 2],
+                                              const T (&wr)[Shape<SS>::NP], int lane, int gx0, int nx) {
+  using TL = Tile<T>;
+  constexpr int V = TL::V, TX = TL::TX, HV = TL::HV, RY = TL::RY, NP = Shape<SS>::NP;
+  T W[3][RY + 2][V + 2];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int dk = d - 1;
+    if (!NZ && dk != 0) continue;
+#pragma unroll
+    for (int t = 0; t < RY + 2; ++t) {
+      bool need = false;
+#pragma unroll
+      for (int dj = -1; dj <= 1; ++dj)
+        if (shape_uses<SS>(dk, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
+      if (!need) continue;
+      const T* row = pl[d] + srow[t];
+      T c[V];
+      ld_vec<T, V>(c, row + HV + lane * V);
+#pragma unroll
+      for (int k = 0; k < V; ++k) W[d][t][k + 1] = c[k];
+      if (shape_uses_x_halo<SS>(dk)) {
+        T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+        T right = __shfl_down_sync(0xffffffffu, c[0], 1);
+        if (lane == 0) left = row[HV - 1];
+        if (lane == 31) right = row[HV + TX];
+        W[d][t][0] = left;
+        W[d][t][V + 1] = right;
+        if constexpr (EDGE) {
+          if (gx0 == 0) W[d][t][0] = W[d][t][1];
+#pragma unroll
+          for (int c2 = 1; c2 < V + 2; ++c2)
+            if (gx0 - 1 + c2 >= nx) W[d][t][c2] = W[d][t][c2 - 1];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      T acc;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const int di = Shape<SS>::off(q, 0), dj = Shape<SS>::off(q, 1), dk = Shape<SS>::off(q, 2);
+        const T v = W[dk + 1][r + 1 + dj][k + 1 + di];
+        acc = (q == 0) ? mul_rn(wr[q], v) : fma_rn(wr[q], v, acc);
+      }
+      out[r][k] = acc;
+    }
+  }
+}
+
 // K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: accumulate the
 // actual checksums.  INJ: apply this launch's scheduled bit-flips.
 template <typename T, int S, bool CHK, bool INJ>
@@ -99,13 +183,16 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
              const __grid_constant__ SweepParams p) {
   using TL = Tile<T>;
   constexpr int V = TL::V, TX = TL::TX, HV = TL::HV, HX = TL::HX, RY = TL::RY, TY = TL::TY;
-  constexpr int NS = TL::NS, NSP = TL::NSP, WARPS = TL::WARPS;
+  constexpr int NS = TL::NS, NSP = TL::NSP, WARPS = TL::WARPS, ROWS = TL::ROWS;
+  constexpr int TSTR = TL::T_STRIDE / (int)sizeof(T), PSTR = TL::P_STRIDE / (int)sizeof(T);
   constexpr bool GEN = (S == SHAPE_GENERIC);
-  constexpr bool NZ = GEN ? true : shape_needs_z<GEN ? SHAPE_HOTSPOT7 : S>();
+  constexpr int SS = GEN ? SHAPE_HOTSPOT7 : S;   // any defined shape for the GEN instantiation
+  constexpr bool NZ = GEN ? true : shape_needs_z<SS>();
+  constexpr int NP = GEN ? 1 : Shape<SS>::NP;
 
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // shared memory: derived from the __shared__ array so every access is LDS/STS
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sT = reinterpret_cast<T*>(base);
   T* sP = reinterpret_cast<T*>(base + NS * TL::T_STRIDE);
   double* sPart = reinterpret_cast<double*>(base + NS * TL::T_STRIDE + NSP * TL::P_STRIDE);
@@ -121,6 +208,13 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
   const int nT = (NZ ? ze + 1 : ze) - q0;
   const int nZ = ze - zs;
   const bool hasP = p.field_src >= 0;
+  const bool xedge = (x0 == 0) || (x0 + TX >= nx);            // clamp / ragged columns
+  const bool full = (x0 + TX <= nx) && (y0 + TY <= ny);       // no masked cells
+  const int64_t px = p.px;
+  T* const out_base = reinterpret_cast<T*>(p.out);
+  double* const Ag = p.A;
+  double* const Bg = p.B;
+  T* const exl = reinterpret_cast<T*>(p.EX);
 
   if (tid == 0) {
     prefetch_tmap(&tm_u);
@@ -133,13 +227,13 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
   auto issue_T = [&](int i) {
     const int st = i % NS;
     mbar_arrive_expect_tx(&barT[st], TL::T_BYTES);
-    tma_load_3d(sT + st * (TL::T_STRIDE / (int)sizeof(T)), &tm_u, &barT[st], x0 - HV, y0 - 1,
+    tma_load_3d(sT + st * TSTR, &tm_u, &barT[st], x0 - HV, y0 - 1,
                 zmap(q0 + i, zc, p.has_lo, p.has_hi));
   };
   auto issue_P = [&](int i) {
     const int st = i % NSP;
     mbar_arrive_expect_tx(&barP[st], TL::P_BYTES);
-    tma_load_3d(sP + st * (TL::P_STRIDE / (int)sizeof(T)), &tm_src, &barP[st], x0, y0, zs + i);
+    tma_load_3d(sP + st * PSTR, &tm_src, &barP[st], x0, y0, zs + i);
   };
   if (tid == 0) {
     for (int i = 0; i < NS && i < nT; ++i) issue_T(i);
@@ -147,13 +241,18 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
       for (int i = 0; i < NSP && i < nZ; ++i) issue_P(i);
   }
 
-  // per-thread geometry
+  // per-thread geometry, loop invariant
   const int gx0 = x0 + lane * V;
   const int ry0 = warp * RY;
   const int gyb = y0 + ry0;
-  int srow[RY + 2];  // staged row of input row gyb - 1 + t, clamped
+  int srow[RY + 2];  // staged row (x HX) of input row gyb - 1 + t, clamped in y
 #pragma unroll
-  for (int t = 0; t < RY + 2; ++t) srow[t] = max(0, min(gyb - 1 + t, ny - 1)) - y0 + 1;
+  for (int t = 0; t < RY + 2; ++t) srow[t] = (max(0, min(gyb - 1 + t, ny - 1)) - y0 + 1) * HX;
+  T wr[NP];
+  if constexpr (!GEN) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) wr[q] = pw<T>(p, q);
+  }
 
   for (int z = zs; z < ze; ++z) {
     const int it = z - zs;
@@ -163,69 +262,20 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
       for (int d = 0; d < 3; ++d) {
         const int i = it + d;
         mbar_wait(&barT[i % NS], (i / NS) & 1);
-        pl[d] = sT + (i % NS) * (TL::T_STRIDE / (int)sizeof(T));
+        pl[d] = sT + (i % NS) * TSTR;
       }
     } else {
       mbar_wait(&barT[it % NS], (it / NS) & 1);
-      pl[0] = pl[2] = nullptr;
-      pl[1] = sT + (it % NS) * (TL::T_STRIDE / (int)sizeof(T));
+      pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
     }
-    const T* ps = sP + (it % NSP) * (TL::P_STRIDE / (int)sizeof(T));
+    const T* ps = sP + (it % NSP) * PSTR;
     if (hasP) mbar_wait(&barP[it % NSP], (it / NSP) & 1);
 
     T out[RY][V];
     if constexpr (!GEN) {
-      constexpr int NP = Shape<S>::NP;
-      T W[3][RY + 2][V + 2];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const int dk = d - 1;
-        if (!NZ && dk != 0) continue;
-#pragma unroll
-        for (int t = 0; t < RY + 2; ++t) {
-          bool need = false;
-#pragma unroll
-          for (int dj = -1; dj <= 1; ++dj)
-            if (shape_uses<S>(dk, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
-          if (!need) continue;
-          const T* row = pl[d] + srow[t] * HX;
-          T c[V];
-          ld_vec<T, V>(c, row + HV + lane * V);
-#pragma unroll
-          for (int k = 0; k < V; ++k) W[d][t][k + 1] = c[k];
-          if (shape_uses_x_halo<S>(dk)) {
-            T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
-            T right = __shfl_down_sync(0xffffffffu, c[0], 1);
-            if (lane == 0) left = row[HV - 1];
-            if (lane == 31) right = row[HV + TX];
-            W[d][t][0] = left;
-            W[d][t][V + 1] = right;
-            if (gx0 == 0) W[d][t][0] = W[d][t][1];
-            if (gx0 + V >= nx) {
-#pragma unroll
-              for (int c2 = 1; c2 < V + 2; ++c2)
-                if (gx0 - 1 + c2 >= nx) W[d][t][c2] = W[d][t][c2 - 1];
-            }
-          }
-        }
-      }
-      T wr[NP];
-#pragma unroll
-      for (int q = 0; q < NP; ++q) wr[q] = (T)p.w[q];
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          T acc;
-#pragma unroll
-          for (int q = 0; q < NP; ++q) {
-            const int di = Shape<S>::off(q, 0), dj = Shape<S>::off(q, 1), dk = Shape<S>::off(q, 2);
-            const T v = W[dk + 1][r + 1 + dj][k + 1 + di];
-            acc = (q == 0) ? mul_rn(wr[q], v) : fma_rn(wr[q], v, acc);
-          }
-          out[r][k] = acc;
-        }
-      }
+      // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
+      if (xedge) stencil_layer<T, SS, NZ, true>(out, pl, srow, wr, lane, gx0, nx);
+      else stencil_layer<T, SS, NZ, false>(out, pl, srow, wr, lane, gx0, nx);
     } else {
       // generic radius-1 point list: runtime offsets, identical FMA chain
 #pragma unroll
@@ -236,10 +286,10 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
           for (int q = 0; q < p.npoints; ++q) {
             const int di = p.di[q], dj = p.dj[q], dk = p.dk[q];
             const T* pp = dk < 0 ? pl[0] : (dk > 0 ? pl[2] : pl[1]);
-            const int sr = max(0, min(gyb + r + dj, ny - 1)) - y0 + 1;
+            const int sr = (max(0, min(gyb + r + dj, ny - 1)) - y0 + 1) * HX;
             const int sc = max(0, min(gx0 + k + di, nx - 1)) - x0 + HV;
-            const T v = pp[sr * HX + sc];
-            const T w = (T)p.w[q];
+            const T v = pp[sr + sc];
+            const T w = pw<T>(p, q);
             acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
           }
           out[r][k] = acc;
@@ -248,7 +298,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
     }
     // constant term C of Eq. 1: sources in order
     for (int q = 0; q < p.nsources; ++q) {
-      const T cf = (T)p.coef[q];
+      const T cf = pcoef<T>(p, q);
       if (q == p.field_src) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -258,7 +308,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
           for (int k = 0; k < V; ++k) out[r][k] = fma_rn(cf, pv[k], out[r][k]);
         }
       } else {
-        const T sv = (T)p.scalar[q];
+        const T sv = pscal<T>(p, q);
 #pragma unroll
         for (int r = 0; r < RY; ++r)
 #pragma unroll
@@ -277,14 +327,23 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
       }
     }
     // store (128-bit where the vector is whole)
-    T* obase = reinterpret_cast<T*>(p.out) + (size_t)(z + 1) * p.plane;
+    T* obase = out_base + (size_t)(z + 1) * p.plane + (size_t)gyb * px + gx0;
+    using VT = typename Vec<T>::type;
+    if (full) {
 #pragma unroll
-    for (int r = 0; r < RY; ++r) {
-      const int gy = gyb + r;
-      if (gy < ny) {
-        T* o = obase + (size_t)gy * p.px + gx0;
+      for (int r = 0; r < RY; ++r) {
+        VT v;
+        T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) e[k] = out[r][k];
+        *reinterpret_cast<VT*>(obase + (size_t)r * px) = v;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        if (gyb + r >= ny) continue;
+        T* o = obase + (size_t)r * px;
         if (gx0 + V <= nx) {
-          using VT = typename Vec<T>::type;
           VT v;
           T* e = reinterpret_cast<T*>(&v);
 #pragma unroll
@@ -297,26 +356,29 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
         }
       }
     }
-    double cs[V];
-    if constexpr (CHK) {
-      double rs[RY];
-#pragma unroll
-      for (int k = 0; k < V; ++k) cs[k] = 0.0;
+    // ledger for Theorem 1's beta terms of the next check: the x-edge columns
+    if (exl && xedge) {
+      const size_t lay = (size_t)(z + 1) * ny;
+      const size_t side = (size_t)(zc + 2) * ny;
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
-        rs[r] = 0.0;
-        const bool vy = gyb + r < ny;
+        const int gy = gyb + r;
+        if (gy >= ny) continue;
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          const double d = (vy && gx0 + k < nx) ? (double)out[r][k] : 0.0;
-          rs[r] += d;
-          cs[k] += d;
+          if (gx0 + k == 0) exl[lay + gy] = out[r][k];
+          if (gx0 + k == nx - 1) exl[side + lay + gy] = out[r][k];
         }
       }
+    }
+    if constexpr (CHK) {
+      double rs[RY], cs[V];
+      if (full) partial_sums<T, true>(out, rs, cs, gyb, gx0, nx, ny);
+      else partial_sums<T, false>(out, rs, cs, gyb, gx0, nx, ny);
       // b^s_y += sum over this tile's columns (Eq. 3)
       const double tot = row_reduce<RY>(rs, lane);
       const int gy = gyb + row_of_lane<RY>(lane);
-      if (final_lane<RY>(lane) && gy < ny) atomicAdd(&p.B[(size_t)(z + 1) * ny + gy], tot);
+      if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(z + 1) * ny + gy], tot);
       __syncthreads();  // the previous layer's column partials have been consumed
 #pragma unroll
       for (int k = 0; k < V; ++k) sPart[warp * TX + lane * V + k] = cs[k];
@@ -330,10 +392,10 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
     if constexpr (CHK) {
       // a^s_x += sum over this tile's rows (Eq. 2)
       if (tid < TX) {
-        double s = 0.0;
+        double s = sPart[tid];
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) s += sPart[w * TX + tid];
-        if (x0 + tid < nx) atomicAdd(&p.A[(size_t)(z + 1) * nx + x0 + tid], s);
+        for (int w = 1; w < WARPS; ++w) s += sPart[w * TX + tid];
+        if (x0 + tid < nx) atomicAdd(&Ag[(size_t)(z + 1) * nx + x0 + tid], s);
       }
     }
   }

@@ -82,7 +82,8 @@ def test_workspace_size_sane(L):
     (dict(mode=7), abft.ABFT_EINVAL),
     (dict(bc=abft.ABFT_BC_PERIODIC), abft.ABFT_EUNSUPPORTED),
     (dict(z_begin=1, z_count=2), abft.ABFT_EINVAL),
-    (dict(nranks=2, rank=0, z_count=2), abft.ABFT_EINVAL),   # no NCCL id
+    (dict(nranks=2, rank=1, z_count=2), abft.ABFT_EINVAL),   # rank 1 cannot own layer 0
+    (dict(nranks=2, rank=0, z_count=4), abft.ABFT_EINVAL),   # rank 0 of 2 owns every layer
 ])
 def test_workspace_size_validates(L, kw, code):
     c, keep = _cfg(**kw)

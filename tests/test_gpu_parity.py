@@ -172,3 +172,74 @@ def test_cfg4_full_size_sampled_and_properties():
     st.destroy()
     rel = ((uf - uc).abs() / uc.abs()).max().item()
     assert rel < 1e-2, rel   # undetected low-bit flips diffuse; detected ones are repaired
+
+
+# ---- z-slab decomposition on one GPU (local group: device-copy halos) --------
+
+def _split(nz, G, uneven):
+    if uneven and G == 2:
+        return [(0, nz // 2 - 1), (nz // 2 - 1, nz - nz // 2 + 1)]
+    base = [nz // G + (1 if i < nz % G else 0) for i in range(G)]
+    out, z = [], 0
+    for c in base:
+        out.append((z, c))
+        z += c
+    return out
+
+
+def _group_run(p, G, faults, uneven=False):
+    from paper_1909_00709_b200 import abft
+    dev = torch.device("cuda:0")
+    u0 = field_u0(p, dev)
+    P = field_power(p, dev)
+    sts = []
+    for i, (z0, zc) in enumerate(_split(p.nz, G, uneven)):
+        st = abft.from_problem(p, u0[z0:z0 + zc].contiguous(),
+                               None if P is None else P[z0:z0 + zc].contiguous(), device=dev,
+                               stream=torch.cuda.Stream(dev), z_begin=z0, z_count=zc, rank=i,
+                               nranks=G)
+        st.set_faults(faults)
+        sts.append(st)
+    abft.group(sts)
+    status = abft.step_group(sts, p.sweeps)
+    u = np.concatenate([s.read_field().cpu().numpy() for s in sts])
+    recs = sum((s.records() for s in sts), [])
+    stats = [s.stats() for s in sts]
+    AB = [s.checksums() for s in sts]
+    A = np.concatenate([a.numpy() for a, b in AB])
+    B = np.concatenate([b.numpy() for a, b in AB])
+    for s in sts:
+        s.destroy()
+    return dict(u=u, records=recs, stats=stats, status=status, A=A, B=B)
+
+
+@pytest.mark.parametrize("G,uneven", [(2, False), (2, True), (3, False), (4, False)])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_slab_group_equals_oracle(G, uneven, mode):
+    # per-layer arithmetic does not depend on the partition, so
+    # any z-slab decomposition is bitwise identical to the single domain.
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=mode, delta=7)
+    faults = fault_schedule(p)
+    faults += [Fault(9, 5, 3, 4, 30), Fault(9, 6, 70, 90, 29)]   # next to a slab face
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, G, faults, uneven)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+    assert np.array_equal(g["A"], o["A"]) and np.array_equal(g["B"], o["B"])
+    for s in g["stats"]:
+        for k in ("sweeps", "rollbacks", "windows", "persistent"):
+            assert s[k] == o["stats"][k], (k, s, o["stats"])
+    for k in ("detections", "corrected", "located"):
+        assert sum(s[k] for s in g["stats"]) == o["stats"][k]
+
+
+def test_slab_group_fp64_box27_offline():
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg5", nx=70, ny=33, nz=9, sweeps=15, nfaults=6)
+    faults = fault_schedule(p)
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, 3, faults)
+    rel = np.abs(g["u"] - o["u"]) / np.abs(o["u"])
+    assert rel.max() <= 1e-12
+    assert_records_equal(g, o, exact_values=False, rtol=1e-12)

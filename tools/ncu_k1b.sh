@@ -1,0 +1,5 @@
+set -x
+B="python tools/exp_k1.py base"
+$B > gpurun_out/plain_exp.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k1_sweep -s 8 -c 1 -o gpurun_out/k1prot3 $B > gpurun_out/ncu_a.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k1_sweep -s 50 -c 1 -o gpurun_out/k1unprot3 $B > gpurun_out/ncu_b.log 2>&1
