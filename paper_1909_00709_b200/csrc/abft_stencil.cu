@@ -360,6 +360,9 @@ int sweep_checked(abft_stencil* h, int src, int dst, double* A, double* B, const
                   int64_t sweep) {
   int r = launch_k1(h, src, dst, A, B, true, sweep);
   if (r) return r;
+#ifdef ABFT_EXP_NO_K2  // experiment builds only (tools/exp_build.py): K1 cost in isolation
+  return ABFT_OK;
+#endif
   return launch_check(h, ck);
 }
 

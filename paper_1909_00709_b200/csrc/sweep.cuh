@@ -378,7 +378,11 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
       // b^s_y += sum over this tile's columns (Eq. 3)
       const double tot = row_reduce<RY>(rs, lane);
       const int gy = gyb + row_of_lane<RY>(lane);
+      #ifdef ABFT_EXP_NO_RED  // experiment builds only: partial sums without the L2 reductions
+      if (final_lane<RY>(lane) && gy < ny && tot == -1.2345) Bg[gy] = tot;
+#else
       if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(z + 1) * ny + gy], tot);
+#endif
       __syncthreads();  // the previous layer's column partials have been consumed
 #pragma unroll
       for (int k = 0; k < V; ++k) sPart[warp * TX + lane * V + k] = cs[k];
@@ -395,7 +399,11 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
         double s = sPart[tid];
 #pragma unroll
         for (int w = 1; w < WARPS; ++w) s += sPart[w * TX + tid];
+        #ifdef ABFT_EXP_NO_RED
+        if (x0 + tid < nx && s == -1.2345) Ag[tid] = s;
+#else
         if (x0 + tid < nx) atomicAdd(&Ag[(size_t)(z + 1) * nx + x0 + tid], s);
+#endif
       }
     }
   }
