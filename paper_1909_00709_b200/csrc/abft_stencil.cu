@@ -80,16 +80,17 @@ EncodeTiledFn encode_fn() {
 }
 
 bool encode3d(CUtensorMap* m, int dtype, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-              uint64_t pitch_bytes, uint64_t layer_bytes, uint32_t b0, uint32_t b1) {
+              uint64_t pitch_bytes, uint64_t layer_bytes, uint32_t b0, uint32_t b1, uint32_t b2 = 1,
+              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {pitch_bytes, layer_bytes};
-  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, dtype == ABFT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                   3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -208,7 +209,12 @@ struct abft_stencil {
   int field_src = -1;
   cudaStream_t stream = nullptr;
   CUtensorMap tm_u[3];
-  CUtensorMap tm_src;
+  // y-march K1 (3D shapes): (x, z) slice boxes, persistent grid
+  bool ymarch = false;
+  CUtensorMap tm_uy[3];
+  CUtensorMap tm_srcy;
+  K1Geometry geoy;
+  dim3 gridy;
   int shape = SHAPE_GENERIC;
   K1Geometry geo;
   dim3 grid1;
@@ -284,7 +290,10 @@ int match_shape(const abft_config* c) {
         return false;
     return true;
   };
-  if (same(Shape<SHAPE_HOTSPOT7>{})) return SHAPE_HOTSPOT7;
+  if (same(Shape<SHAPE_HOTSPOT7>{})) {
+    const bool fs = c->nsources == 2 && c->sources[0].field && !c->sources[1].field;
+    return fs ? SHAPE_HOTSPOT7_FS : SHAPE_HOTSPOT7;
+  }
   if (same(Shape<SHAPE_FIG2_5PT>{})) return SHAPE_FIG2_5PT;
   if (same(Shape<SHAPE_BOX27>{})) return SHAPE_BOX27;
   return SHAPE_GENERIC;
@@ -330,9 +339,15 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk,
   const bool inj = p.nfaults > 0;
   h->executed++;
   cudaEvent_t* pe = prof_begin(h, 1);
-  cudaError_t e = h->cfg.dtype == ABFT_F32
-                      ? launch_k1_f32(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], h->tm_src, p)
-                      : launch_k1_f64(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], h->tm_src, p);
+  cudaError_t e;
+  if (h->ymarch)
+    e = h->cfg.dtype == ABFT_F32
+            ? launch_k1y_f32(h->shape, chk, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p)
+            : launch_k1y_f64(h->shape, chk, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p);
+  else
+    e = h->cfg.dtype == ABFT_F32
+            ? launch_k1_f32(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], p)
+            : launch_k1_f64(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], p);
   prof_end(h, pe);
   h->launches++;
   CK(e);
@@ -733,11 +748,6 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
     if (!encode3d(&h->tm_u[b], cfg->dtype, h->fb[b], nx, ny, zc + 2, L.px * esz, L.plane * esz,
                   h->geo.tile_x + 2 * HV, h->geo.tile_y + 2))
       return fail(ABFT_ECUDA);
-  memset(&h->tm_src, 0, sizeof(h->tm_src));
-  if (h->field_src >= 0 &&
-      !encode3d(&h->tm_src, cfg->dtype, const_cast<void*>(h->src_field), nx, ny, zc, h->src_px * esz,
-                h->src_px * ny * esz, h->geo.tile_x, h->geo.tile_y))
-    return fail(ABFT_ECUDA);
 
   // launch geometry: z-chunks so the grid is >= ~8 waves of resident CTAs
   h->shape = match_shape(cfg);
@@ -753,10 +763,45 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
   h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
 
+  // 3D point lists on slabs of >= 16 layers run the y-march K1 (sweep_y.cuh):
+  // a_x accumulates in registers along y, no tail wave.  ABFT_K1_MARCH=z|y
+  // overrides (tests of both traversals).
+  bool needs_z = false;
+  for (int q = 0; q < cfg->npoints; ++q) needs_z |= cfg->points[q].dk != 0;
+  h->ymarch = false;   // measured slower on cfg4 (profiles/r01): opt-in only
+  if (const char* e = getenv("ABFT_K1_MARCH")) {
+    if (e[0] == 'z') h->ymarch = false;
+    if (e[0] == 'y') h->ymarch = needs_z;
+  }
+  int ntx = 0, ntz = 0;
+  if (h->ymarch) {
+    h->geoy = k1y_geometry(cfg->dtype);
+    for (int b = 0; b < h->nbuf; ++b)
+      if (!encode3d(&h->tm_uy[b], cfg->dtype, h->fb[b], nx, ny, zc + 2, L.px * esz, L.plane * esz,
+                    h->geoy.tile_x + 2 * HV, 1, h->geoy.tile_y + 2,
+                    getenv("ABFT_Y_PROMO256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                              : CU_TENSOR_MAP_L2_PROMOTION_NONE))
+        return fail(ABFT_ECUDA);
+    memset(&h->tm_srcy, 0, sizeof(h->tm_srcy));
+    if (h->field_src >= 0 &&
+        !encode3d(&h->tm_srcy, cfg->dtype, const_cast<void*>(h->src_field), nx, ny, zc, h->src_px * esz,
+                  h->src_px * ny * esz, h->geoy.tile_x, 1, h->geoy.tile_y))
+      return fail(ABFT_ECUDA);
+    ntx = (int)((nx + h->geoy.tile_x - 1) / h->geoy.tile_x);
+    ntz = (int)((zc + h->geoy.tile_y - 1) / h->geoy.tile_y);
+    const int occ = cfg->dtype == ABFT_F32 ? k1y_occ_f32(h->shape) : k1y_occ_f64(h->shape);
+    const int64_t rows = (int64_t)ntx * ntz * ny;
+    h->gridy = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)nsm * occ)));
+  }
+
   // parameter blocks (weights and coefficients rounded to the dtype)
   SweepParams& sp = h->sp;
   memset(&sp, 0, sizeof(sp));
   sp.nx = (int)nx; sp.ny = (int)ny; sp.zc = (int)zc; sp.zchunk = h->zchunk;
+  sp.ntx = ntx; sp.ntz = ntz;
+  sp.src = h->src_field;
+  sp.spx = h->src_px;
+  sp.splane = h->src_px * ny;
   sp.px = L.px; sp.plane = L.plane; sp.has_lo = h->has_lo; sp.has_hi = h->has_hi;
   sp.npoints = cfg->npoints; sp.nsources = cfg->nsources; sp.field_src = h->field_src;
   for (int q = 0; q < cfg->npoints; ++q) {
@@ -1017,7 +1062,10 @@ int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_n, dou
   if (k1_n) *k1_n = n[1];
   if (k2_ms) *k2_ms = t[2];
   if (k2_n) *k2_n = n[2];
-  if (geo) {
+  if (geo && h->ymarch) {   // persistent y-march: grid, threads, smem, layers per tile
+    geo[0] = h->gridy.x; geo[1] = 1; geo[2] = 1;
+    geo[3] = h->geoy.threads; geo[4] = h->geoy.smem; geo[5] = h->geoy.tile_y;
+  } else if (geo) {
     geo[0] = h->grid1.x; geo[1] = h->grid1.y; geo[2] = h->grid1.z;
     geo[3] = h->geo.threads; geo[4] = h->geo.smem; geo[5] = h->zchunk;
   }

@@ -178,66 +178,75 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
   }
 }
 
-// K2.  grid (zc, ceil((nx + ny) / kCheckThreads)): every thread owns one entry
-// of a' or b' of layer blockIdx.x; the CTA that completes a layer last (per-layer
-// counter) locates, corrects and records (Eq. 8, fig.correction).
+// K2.  One CTA per z-layer (grid = zc): every thread predicts / compares
+// KU entries of a' and b' per round with all their loads in flight; the
+// layer's flags meet in shared memory, so the same CTA then locates, corrects
+// and records (Eq. 8, fig.correction) -- no cross-CTA handshake.
+constexpr int kCheckUnroll = 4;
 template <typename T, int S>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
   const int z = blockIdx.x, bz = z + 1;
-  const int nx = p.nx, ny = p.ny, zc = p.zc;
+  const int nx = p.nx, ny = p.ny, ne = nx + ny;
   const int tid = threadIdx.x;
   LayerSummary* L = &p.summ[z];
-  __shared__ int s_last;
+  __shared__ int s_na, s_nb, s_xk, s_yk;
+  __shared__ double s_pa, s_pb;
   __shared__ double red[kCheckThreads / 32];
+  int na, nb, xk, yk;
+  double pa, pb;
   if (!(p.flags & CK_FROM_SUMMARY)) {
-    const int e = blockIdx.y * kCheckThreads + tid;
-    if (e < nx) {
-      const double pa = predict_entry<T, S, true>(p, z, e);
-      if (p.flags & CK_STORE_PRED) p.PAo[(size_t)bz * nx + e] = pa;
-      if ((p.flags & CK_COMPARE) && flag_rel(pa, p.Ac[(size_t)bz * nx + e], p.eps)) {
-        atomicAdd(&L->na, 1);
-        atomicMax(&L->xk, 0x7fffffff - e);
-        L->pa = pa;
-        __threadfence();
+    if (tid == 0) { s_na = 0; s_nb = 0; s_xk = 0; s_yk = 0; s_pa = 0.0; s_pb = 0.0; }
+    __syncthreads();
+    for (int e0 = 0; e0 < ne; e0 += kCheckThreads * kCheckUnroll) {
+      double pr[kCheckUnroll];
+#pragma unroll
+      for (int u = 0; u < kCheckUnroll; ++u) {
+        const int e = e0 + u * kCheckThreads + tid;
+        pr[u] = 0.0;
+        if (e < nx) pr[u] = predict_entry<T, S, true>(p, z, e);
+        else if (e < ne) pr[u] = predict_entry<T, S, false>(p, z, e - nx);
       }
-      if (p.zA) p.zA[(size_t)bz * nx + e] = 0.0;   // generation of the next sweep
-    } else if (e < nx + ny) {
-      const int y = e - nx;
-      const double pb = predict_entry<T, S, false>(p, z, y);
-      if (p.flags & CK_STORE_PRED) p.PBo[(size_t)bz * ny + y] = pb;
-      if ((p.flags & CK_COMPARE) && flag_rel(pb, p.Bc[(size_t)bz * ny + y], p.eps)) {
-        atomicAdd(&L->nb, 1);
-        atomicMax(&L->yk, 0x7fffffff - y);
-        L->pb = pb;
-        __threadfence();
+#pragma unroll
+      for (int u = 0; u < kCheckUnroll; ++u) {
+        const int e = e0 + u * kCheckThreads + tid;
+        if (e < nx) {
+          if (p.flags & CK_STORE_PRED) p.PAo[(size_t)bz * nx + e] = pr[u];
+          if ((p.flags & CK_COMPARE) && flag_rel(pr[u], p.Ac[(size_t)bz * nx + e], p.eps)) {
+            atomicAdd(&s_na, 1);
+            atomicMax(&s_xk, 0x7fffffff - e);
+            s_pa = pr[u];
+          }
+          if (p.zA) p.zA[(size_t)bz * nx + e] = 0.0;   // generation of sweep s + 2
+        } else if (e < ne) {
+          const int y = e - nx;
+          if (p.flags & CK_STORE_PRED) p.PBo[(size_t)bz * ny + y] = pr[u];
+          if ((p.flags & CK_COMPARE) && flag_rel(pr[u], p.Bc[(size_t)bz * ny + y], p.eps)) {
+            atomicAdd(&s_nb, 1);
+            atomicMax(&s_yk, 0x7fffffff - y);
+            s_pb = pr[u];
+          }
+          if (p.zB) p.zB[(size_t)bz * ny + y] = 0.0;
+        }
       }
-      if (p.zB) p.zB[(size_t)bz * ny + y] = 0.0;
     }
     if (!(p.flags & CK_COMPARE)) return;
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(&L->done, 1) == (int)gridDim.y - 1;
+    na = s_na; nb = s_nb; xk = s_xk; yk = s_yk; pa = s_pa; pb = s_pb;
+    if (p.flags & CK_SUMMARY) {   // explicit check(): keep the summary for correct()
+      if (tid == 0) {
+        L->na = na; L->nb = nb; L->xk = xk; L->yk = yk; L->pa = pa; L->pb = pb;
+        if (na) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_a), (unsigned long long)na);
+        if (nb) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_b), (unsigned long long)nb);
+      }
+      return;
     }
+  } else {
+    na = L->na; nb = L->nb; xk = L->xk; yk = L->yk; pa = L->pa; pb = L->pb;
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
+    if (tid == 0) { L->na = 0; L->nb = 0; L->xk = 0; L->yk = 0; }
   }
-  // ---- this CTA sees the whole layer's compare
-  const int na = *(volatile int*)&L->na, nb = *(volatile int*)&L->nb;
-  const int x0 = na ? 0x7fffffff - *(volatile int*)&L->xk : -1;
-  const int y0 = nb ? 0x7fffffff - *(volatile int*)&L->yk : -1;
-  const double pa = *(volatile double*)&L->pa, pb = *(volatile double*)&L->pb;
-  if (p.flags & CK_SUMMARY) {   // explicit check(): keep the summary for correct()
-    if (tid == 0) {
-      L->done = 0;
-      if (na) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_a), (unsigned long long)na);
-      if (nb) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->flag_b), (unsigned long long)nb);
-    }
-    return;
-  }
-  __syncthreads();
-  if (tid == 0) { L->na = 0; L->nb = 0; L->xk = 0; L->yk = 0; L->done = 0; }
+  const int x0 = na ? 0x7fffffff - xk : -1;
+  const int y0 = nb ? 0x7fffffff - yk : -1;
   finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
 }
 

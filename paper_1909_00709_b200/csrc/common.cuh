@@ -21,7 +21,8 @@ constexpr int kRecordCap = 4096;
 // part of the numeric contract).  Shapes whose point ORDER is known at compile
 // time get a register-blocked kernel; any other radius-1 list runs the generic
 // kernel (runtime offsets, same arithmetic).
-enum ShapeId { SHAPE_GENERIC = 0, SHAPE_FIG2_5PT = 1, SHAPE_HOTSPOT7 = 2, SHAPE_BOX27 = 3 };
+enum ShapeId { SHAPE_GENERIC = 0, SHAPE_FIG2_5PT = 1, SHAPE_HOTSPOT7 = 2, SHAPE_BOX27 = 3,
+               SHAPE_HOTSPOT7_FS = 4 /* HotSpot points + sources [field, scalar] */ };
 
 template <int S> struct Shape;
 // fig.sweep: c, w(x-1), e(x+1), s(y+1), n(y-1)
@@ -41,6 +42,7 @@ template <> struct Shape<SHAPE_HOTSPOT7> {
     return t[p][a];
   }
 };
+template <> struct Shape<SHAPE_HOTSPOT7_FS> : Shape<SHAPE_HOTSPOT7> {};
 // 27-point box, dk outer, dj middle, di inner, ascending (BASELINE.json configs[4])
 template <> struct Shape<SHAPE_BOX27> {
   static constexpr int NP = 27;
@@ -49,22 +51,34 @@ template <> struct Shape<SHAPE_BOX27> {
   }
 };
 
-template <int S> __host__ __device__ constexpr bool shape_needs_z() {
-  for (int p = 0; p < Shape<S>::NP; ++p)
-    if (Shape<S>::off(p, 2) != 0) return true;
+// The helpers take the shape as a type so a kernel can evaluate the same
+// point list with two axes exchanged (SwapYZ: the y-march of sweep_y.cuh
+// stages (x, z) slices and slides along y).
+template <class SH> __host__ __device__ constexpr bool sh_needs_z() {
+  for (int p = 0; p < SH::NP; ++p)
+    if (SH::off(p, 2) != 0) return true;
   return false;
 }
-// does plane dk need input row offset dj (relative to an output row)?
-template <int S> __host__ __device__ constexpr bool shape_uses(int dk, int dj) {
-  for (int p = 0; p < Shape<S>::NP; ++p)
-    if (Shape<S>::off(p, 2) == dk && Shape<S>::off(p, 1) == dj) return true;
+// does staged plane dk need input row offset dj (relative to an output row)?
+template <class SH> __host__ __device__ constexpr bool sh_uses(int dk, int dj) {
+  for (int p = 0; p < SH::NP; ++p)
+    if (SH::off(p, 2) == dk && SH::off(p, 1) == dj) return true;
   return false;
 }
-template <int S> __host__ __device__ constexpr bool shape_uses_x_halo(int dk) {
-  for (int p = 0; p < Shape<S>::NP; ++p)
-    if (Shape<S>::off(p, 2) == dk && Shape<S>::off(p, 0) != 0) return true;
+template <class SH> __host__ __device__ constexpr bool sh_uses_x_halo(int dk) {
+  for (int p = 0; p < SH::NP; ++p)
+    if (SH::off(p, 2) == dk && SH::off(p, 0) != 0) return true;
   return false;
 }
+template <int S> __host__ __device__ constexpr bool shape_needs_z() { return sh_needs_z<Shape<S>>(); }
+
+// the point list of shape S with the y and z axes exchanged (same point order)
+template <int S> struct SwapYZ {
+  static constexpr int NP = Shape<S>::NP;
+  __host__ __device__ static constexpr int off(int p, int a) {
+    return Shape<S>::off(p, a == 1 ? 2 : (a == 2 ? 1 : 0));
+  }
+};
 
 // ------------------------------------------------------------ param blocks
 struct LocalFault { int z, y, x, bit; };  // slab-local layer, row, column
@@ -85,11 +99,11 @@ enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCO
        ST_ROLLBACKS, ST_WINDOWS, ST_PERSIST };
 
 // per-layer summary written by check() and consumed by correct()
-// Zero-initialised; the CTA that finishes a layer last consumes and resets it.
+// Written by an explicit check(), consumed and reset by correct().
 struct LayerSummary {
   int na, nb;      // flagged entries of a (over x) and b (over y)
   int xk, yk;      // max of (INT_MAX - index) over flagged entries: the first flagged index
-  int done;        // CTAs of this layer that finished the compare
+  int spare;
   int pad;
   double pa, pb;   // predicted a'_{x0}, b'_{y0} (meaningful when na == 1 / nb == 1)
 };
@@ -134,6 +148,7 @@ struct CheckParams {
 
 struct SweepParams {
   int nx, ny, zc, zchunk;
+  int ntx, ntz;        // y-march: x-tiles x z-tiles (each ny rows), split over the grid
   int64_t px;          // row pitch of the field buffers (elements)
   int64_t plane;       // layer pitch = px * ny
   int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)
@@ -149,6 +164,8 @@ struct SweepParams {
   float coeff[kMaxSources];
   float scalarf[kMaxSources];
   int field_src;                 // index of the source with a field, -1 if none
+  const void* src;               // that field, [zc][ny][spx] (16-byte aligned rows)
+  int64_t spx, splane;
   void* EX;            // edge columns of the output: [2][zc+2][ny] (x = 0, x = nx-1), or null
   int nfaults;
   LocalFault faults[kMaxFaultsPerLaunch];
@@ -171,6 +188,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(

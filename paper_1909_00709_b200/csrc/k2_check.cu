@@ -2,6 +2,7 @@
 #include "check.cuh"
 #include "launch.h"
 #include "sweep.cuh"
+#include "sweep_y.cuh"  // YTile geometry only
 
 namespace abft {
 
@@ -10,11 +11,17 @@ K1Geometry k1_geometry(int dtype) {
   return {Tile<double>::TX, Tile<double>::TY, Tile<double>::SMEM, Tile<double>::THREADS};
 }
 
+K1Geometry k1y_geometry(int dtype) {
+  if (dtype == ABFT_F32) return {YTile<float>::TX, YTile<float>::TZ, YTile<float>::SMEM, YTile<float>::THREADS};
+  return {YTile<double>::TX, YTile<double>::TZ, YTile<double>::SMEM, YTile<double>::THREADS};
+}
+
 template <typename T>
 static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
   switch (shape) {
     case SHAPE_FIG2_5PT: k2_check<T, SHAPE_FIG2_5PT><<<g, kCheckThreads, 0, s>>>(p); break;
-    case SHAPE_HOTSPOT7: k2_check<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7:
+    case SHAPE_HOTSPOT7_FS: k2_check<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
     case SHAPE_BOX27: k2_check<T, SHAPE_BOX27><<<g, kCheckThreads, 0, s>>>(p); break;
     default: k2_check<T, SHAPE_GENERIC><<<g, kCheckThreads, 0, s>>>(p); break;
   }
@@ -22,8 +29,7 @@ static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
 }
 
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p) {
-  const int nblk = (p.flags & CK_FROM_SUMMARY) ? 1 : (p.nx + p.ny + kCheckThreads - 1) / kCheckThreads;
-  const dim3 g(zc, nblk);
+  const dim3 g(zc);
   return dtype == ABFT_F32 ? k2_go<float>(shape, g, s, p) : k2_go<double>(shape, g, s, p);
 }
 

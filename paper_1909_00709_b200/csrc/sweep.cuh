@@ -7,15 +7,17 @@
 //  * one CTA owns a TX x TY tile of every layer of a z-chunk and marches up
 //    z; the input layers z-1, z, z+1 (incl. a 1-row / 16-byte x halo) are
 //    staged in shared memory by TMA (cp.async.bulk.tensor.3d) through an
-//    NS-deep mbarrier ring, the source field C (HotSpot power) through its own
-//    ring, so every HBM byte is read once per sweep by the tile that needs it;
+//    NS-deep mbarrier ring (2 layers in flight); the source field C (HotSpot
+//    power) is read once, straight into registers one layer ahead (128-bit
+//    read-only loads), so every HBM byte is read once per sweep;
 //  * each thread register-blocks V (one 16-byte vector) x RY cells, evaluates
 //    the canonical FMA chain of the stencil (points in the caller's order),
 //    stores with 128-bit coalesced stores;
 //  * the row sums b_y (over x) are reduced across the warp with a transposed
 //    shuffle reduction in fp64, the column sums a_x (over y) across the warps
-//    in shared memory, then one fp64 RED per (tile, row) and (tile, column)
-//    into the L2-resident checksum generation -- no extra HBM traffic;
+//    in shared memory (double-buffered: one CTA barrier per layer, shared with
+//    the ring), then one fp64 RED per (tile, row) and (tile, column) into the
+//    L2-resident checksum generation -- no extra HBM traffic;
 //  * fault injection flips the value after the update and before the
 //    store, so the checksums see the corrupted value (template INJ).
 #pragma once
@@ -29,7 +31,10 @@ template <typename T> struct Tile {
   static constexpr int TX = 32 * V;               // tile width: one vector per lane
   static constexpr int HV = V;                    // x halo per side (keeps 16 B alignment)
   static constexpr int HX = TX + 2 * HV;          // staged row length
-  static constexpr int WARPS = 8;
+#ifndef ABFT_WARPS
+#define ABFT_WARPS 8
+#endif
+  static constexpr int WARPS = ABFT_WARPS;
   static constexpr int THREADS = 32 * WARPS;
 #ifndef ABFT_RY_F32
 #define ABFT_RY_F32 4
@@ -42,13 +47,10 @@ template <typename T> struct Tile {
   static constexpr int ROWS = TY + 2;
   static constexpr int T_BYTES = ROWS * HX * (int)sizeof(T);
   static constexpr int T_STRIDE = (T_BYTES + 127) / 128 * 128;
-  static constexpr int P_BYTES = TX * TY * (int)sizeof(T);
-  static constexpr int P_STRIDE = (P_BYTES + 127) / 128 * 128;
-  static constexpr int NS = ABFT_NS;  // field-layer ring: z-1, z, z+1 + 1 prefetch
-  static constexpr int NSP = 2;   // source-layer ring
-  static constexpr int PART_BYTES = WARPS * TX * 8;
+  static constexpr int NS = ABFT_NS;  // field-layer ring: z-1, z, z+1 + 1 prefetch (5 measured slower)
+  static constexpr int PART_BYTES = 2 * WARPS * TX * 8;   // column partials, double-buffered
   static constexpr int BAR_BYTES = 128;
-  static constexpr int SMEM = NS * T_STRIDE + NSP * P_STRIDE + PART_BYTES + BAR_BYTES + 128;
+  static constexpr int SMEM = NS * T_STRIDE + PART_BYTES + BAR_BYTES + 128;
 };
 
 template <typename T> struct Vec;
@@ -116,17 +118,22 @@ __device__ __forceinline__ void partial_sums(const T (&out)[Tile<T>::RY][Tile<T>
   }
 }
 
-// One layer of one thread: RY x V outputs of Eq. 1 from the staged layers
-// pl[0..2] (z-1, z, z+1), the canonical FMA chain in the shape's point order.
-// EDGE: the tile touches x = 0 or x = nx - 1, so out-of-domain x reads take
-// the clamped value; y is clamped through srow.
-template <typename T, int SS, bool NZ, bool EDGE>
-__device__ __forceinline__ void stencil_layer(T (&out)[Tile<T>::RY][Tile<T>::V], const T* const (&pl)[3],
-                                              const int (&srow)[Tile<T>::RY + 2],
-                                              const T (&wr)[Shape<SS>::NP], int lane, int gx0, int nx) {
-  using TL = Tile<T>;
-  constexpr int V = TL::V, TX = TL::TX, HV = TL::HV, RY = TL::RY, NP = Shape<SS>::NP;
+// One layer of one thread: RY x V outputs of Eq. 1 from the staged planes
+// pl[0..2] (offset -1, 0, +1 along the march axis), the canonical FMA chain in
+// the shape's point order; srow[t] = staged row of input row (first - 1 + t),
+// already clamped or mapped to a halo.  EDGE: the tile touches
+// x = 0 or x = nx - 1, so out-of-domain x reads take the clamped value.
+// SH is the shape seen in the staged coordinates (Shape<S>, or SwapYZ<S> for
+// the y-march): off(q, 2) selects the plane, off(q, 1) the row.
+template <typename T, class SH, int RY, bool NZ, bool EDGE>
+__device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
+                                              const int (&srow)[RY + 2], const T (&wr)[SH::NP],
+                                              int lane, int gx0, int nx) {
+  constexpr int V = 16 / (int)sizeof(T), TX = 32 * V, HV = V, NP = SH::NP;
   T W[3][RY + 2][V + 2];
+  // lanes 0 / 31 need the staged halo element left / right of the tile: every
+  // lane loads one of the two (2 addresses, one wavefront), no divergence
+  const int eoff = lane == 0 ? HV - 1 : HV + TX;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int dk = d - 1;
@@ -136,18 +143,19 @@ __device__ __forceinline__ void stencil_layer(T (&out)[Tile<T>::RY][Tile<T>::V],
       bool need = false;
 #pragma unroll
       for (int dj = -1; dj <= 1; ++dj)
-        if (shape_uses<SS>(dk, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
+        if (sh_uses<SH>(dk, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
       if (!need) continue;
       const T* row = pl[d] + srow[t];
       T c[V];
       ld_vec<T, V>(c, row + HV + lane * V);
 #pragma unroll
       for (int k = 0; k < V; ++k) W[d][t][k + 1] = c[k];
-      if (shape_uses_x_halo<SS>(dk)) {
+      if (sh_uses_x_halo<SH>(dk)) {
+        const T e = row[eoff];
         T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
         T right = __shfl_down_sync(0xffffffffu, c[0], 1);
-        if (lane == 0) left = row[HV - 1];
-        if (lane == 31) right = row[HV + TX];
+        left = lane == 0 ? e : left;
+        right = lane == 31 ? e : right;
         W[d][t][0] = left;
         W[d][t][V + 1] = right;
         if constexpr (EDGE) {
@@ -166,7 +174,7 @@ __device__ __forceinline__ void stencil_layer(T (&out)[Tile<T>::RY][Tile<T>::V],
       T acc;
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        const int di = Shape<SS>::off(q, 0), dj = Shape<SS>::off(q, 1), dk = Shape<SS>::off(q, 2);
+        const int di = SH::off(q, 0), dj = SH::off(q, 1), dk = SH::off(q, 2);
         const T v = W[dk + 1][r + 1 + dj][k + 1 + di];
         acc = (q == 0) ? mul_rn(wr[q], v) : fma_rn(wr[q], v, acc);
       }
@@ -175,17 +183,66 @@ __device__ __forceinline__ void stencil_layer(T (&out)[Tile<T>::RY][Tile<T>::V],
   }
 }
 
+// the source field C (HotSpot power) of layer z for this thread's RY x V
+// cells: read-only 128-bit loads, issued one layer ahead (register prefetch)
+template <typename T, int RY>
+__device__ __forceinline__ void load_src(T (&pv)[RY][16 / sizeof(T)], const SweepParams& p, int z,
+                                         int gyb, int gx0, bool full) {
+  constexpr int V = 16 / (int)sizeof(T);
+  using VT = typename Vec<T>::type;
+  const T* base = reinterpret_cast<const T*>(p.src) + (size_t)z * p.splane + (size_t)gyb * p.spx + gx0;
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const T* q = base + (size_t)r * p.spx;
+    if (full || (gyb + r < p.ny && gx0 + V <= p.nx)) {
+      VT v = __ldg(reinterpret_cast<const VT*>(q));
+      const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int k = 0; k < V; ++k) pv[r][k] = e[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) pv[r][k] = (gyb + r < p.ny && gx0 + k < p.nx) ? __ldg(q + k) : T(0);
+    }
+  }
+}
+
+// the constant term C of Eq. 1 (sources in the caller's order, fma each):
+// FS = the HotSpot pattern [field source, scalar source] with the operands in
+// registers; otherwise the runtime list.
+template <typename T, int RY, bool FS>
+__device__ __forceinline__ void add_sources(T (&out)[RY][16 / sizeof(T)], const T (&pv)[RY][16 / sizeof(T)],
+                                            const SweepParams& p, T c0, T c1, T s1) {
+  constexpr int V = 16 / (int)sizeof(T);
+  if constexpr (FS) {
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int k = 0; k < V; ++k) out[r][k] = fma_rn(c1, s1, fma_rn(c0, pv[r][k], out[r][k]));
+  } else {
+    for (int q = 0; q < p.nsources; ++q) {
+      const T cf = pcoef<T>(p, q);
+      const bool fld = q == p.field_src;
+      const T sv = pscal<T>(p, q);
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int k = 0; k < V; ++k) out[r][k] = fma_rn(cf, fld ? pv[r][k] : sv, out[r][k]);
+    }
+  }
+}
+
 // K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: accumulate the
 // actual checksums.  INJ: apply this launch's scheduled bit-flips.
+// grid (x-tiles, y-tiles, z-chunks); each CTA marches up its z-chunk.
 template <typename T, int S, bool CHK, bool INJ>
-__global__ void __launch_bounds__(Tile<T>::THREADS, 1)
-    k1_sweep(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_src,
-             const __grid_constant__ SweepParams p) {
+__global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
+    k1_sweep(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ SweepParams p) {
   using TL = Tile<T>;
   constexpr int V = TL::V, TX = TL::TX, HV = TL::HV, HX = TL::HX, RY = TL::RY, TY = TL::TY;
-  constexpr int NS = TL::NS, NSP = TL::NSP, WARPS = TL::WARPS, ROWS = TL::ROWS;
-  constexpr int TSTR = TL::T_STRIDE / (int)sizeof(T), PSTR = TL::P_STRIDE / (int)sizeof(T);
+  constexpr int NS = TL::NS, WARPS = TL::WARPS;
+  constexpr int TSTR = TL::T_STRIDE / (int)sizeof(T);
   constexpr bool GEN = (S == SHAPE_GENERIC);
+  constexpr bool FS = (S == SHAPE_HOTSPOT7_FS);
   constexpr int SS = GEN ? SHAPE_HOTSPOT7 : S;   // any defined shape for the GEN instantiation
   constexpr bool NZ = GEN ? true : shape_needs_z<SS>();
   constexpr int NP = GEN ? 1 : Shape<SS>::NP;
@@ -194,11 +251,8 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sT = reinterpret_cast<T*>(base);
-  T* sP = reinterpret_cast<T*>(base + NS * TL::T_STRIDE);
-  double* sPart = reinterpret_cast<double*>(base + NS * TL::T_STRIDE + NSP * TL::P_STRIDE);
-  uint64_t* barT = reinterpret_cast<uint64_t*>(base + NS * TL::T_STRIDE + NSP * TL::P_STRIDE +
-                                               TL::PART_BYTES);
-  uint64_t* barP = barT + NS;
+  double* sPart = reinterpret_cast<double*>(base + NS * TL::T_STRIDE);   // [2][WARPS][TX]
+  uint64_t* barT = reinterpret_cast<uint64_t*>(base + NS * TL::T_STRIDE + TL::PART_BYTES);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = p.nx, ny = p.ny, zc = p.zc;
@@ -206,7 +260,6 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
   const int zs = blockIdx.z * p.zchunk, ze = min(zs + p.zchunk, zc);
   const int q0 = NZ ? zs - 1 : zs;
   const int nT = (NZ ? ze + 1 : ze) - q0;
-  const int nZ = ze - zs;
   const bool hasP = p.field_src >= 0;
   const bool xedge = (x0 == 0) || (x0 + TX >= nx);            // clamp / ragged columns
   const bool full = (x0 + TX <= nx) && (y0 + TY <= ny);       // no masked cells
@@ -218,9 +271,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
 
   if (tid == 0) {
     prefetch_tmap(&tm_u);
-    if (hasP) prefetch_tmap(&tm_src);
     for (int i = 0; i < NS; ++i) mbar_init(&barT[i], 1);
-    for (int i = 0; i < NSP; ++i) mbar_init(&barP[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -230,16 +281,8 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
     tma_load_3d(sT + st * TSTR, &tm_u, &barT[st], x0 - HV, y0 - 1,
                 zmap(q0 + i, zc, p.has_lo, p.has_hi));
   };
-  auto issue_P = [&](int i) {
-    const int st = i % NSP;
-    mbar_arrive_expect_tx(&barP[st], TL::P_BYTES);
-    tma_load_3d(sP + st * PSTR, &tm_src, &barP[st], x0, y0, zs + i);
-  };
-  if (tid == 0) {
+  if (tid == 0)
     for (int i = 0; i < NS && i < nT; ++i) issue_T(i);
-    if (hasP)
-      for (int i = 0; i < NSP && i < nZ; ++i) issue_P(i);
-  }
 
   // per-thread geometry, loop invariant
   const int gx0 = x0 + lane * V;
@@ -253,29 +296,40 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
 #pragma unroll
     for (int q = 0; q < NP; ++q) wr[q] = pw<T>(p, q);
   }
+  T c0 = T(0), c1 = T(0), s1 = T(0);
+  if constexpr (FS) { c0 = pcoef<T>(p, 0); c1 = pcoef<T>(p, 1); s1 = pscal<T>(p, 1); }
+  T pv[RY][V], pn[RY][V];
+  if (hasP) load_src<T, RY>(pn, p, zs, gyb, gx0, full);
 
   for (int z = zs; z < ze; ++z) {
     const int it = z - zs;
     const T* pl[3];
     if (NZ) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const int i = it + d;
-        mbar_wait(&barT[i % NS], (i / NS) & 1);
-        pl[d] = sT + (i % NS) * TSTR;
+      // entries it, it+1 were waited for by the previous layer (or here, first)
+      if (it == 0) {
+        mbar_wait(&barT[0], 0);
+        mbar_wait(&barT[1 % NS], (1 / NS) & 1);
       }
+      mbar_wait(&barT[(it + 2) % NS], ((it + 2) / NS) & 1);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) pl[d] = sT + ((it + d) % NS) * TSTR;
     } else {
       mbar_wait(&barT[it % NS], (it / NS) & 1);
       pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
     }
-    const T* ps = sP + (it % NSP) * PSTR;
-    if (hasP) mbar_wait(&barP[it % NSP], (it / NSP) & 1);
+    if (hasP) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int k = 0; k < V; ++k) pv[r][k] = pn[r][k];
+      if (z + 1 < ze) load_src<T, RY>(pn, p, z + 1, gyb, gx0, full);
+    }
 
     T out[RY][V];
     if constexpr (!GEN) {
       // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
-      if (xedge) stencil_layer<T, SS, NZ, true>(out, pl, srow, wr, lane, gx0, nx);
-      else stencil_layer<T, SS, NZ, false>(out, pl, srow, wr, lane, gx0, nx);
+      if (xedge) stencil_layer<T, Shape<SS>, RY, NZ, true>(out, pl, srow, wr, lane, gx0, nx);
+      else stencil_layer<T, Shape<SS>, RY, NZ, false>(out, pl, srow, wr, lane, gx0, nx);
     } else {
       // generic radius-1 point list: runtime offsets, identical FMA chain
 #pragma unroll
@@ -296,25 +350,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
         }
       }
     }
-    // constant term C of Eq. 1: sources in order
-    for (int q = 0; q < p.nsources; ++q) {
-      const T cf = pcoef<T>(p, q);
-      if (q == p.field_src) {
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          T pv[V];
-          ld_vec<T, V>(pv, ps + (ry0 + r) * TX + lane * V);
-#pragma unroll
-          for (int k = 0; k < V; ++k) out[r][k] = fma_rn(cf, pv[k], out[r][k]);
-        }
-      } else {
-        const T sv = pscal<T>(p, q);
-#pragma unroll
-        for (int r = 0; r < RY; ++r)
-#pragma unroll
-          for (int k = 0; k < V; ++k) out[r][k] = fma_rn(cf, sv, out[r][k]);
-      }
-    }
+    add_sources<T, RY, FS>(out, pv, p, c0, c1, s1);   // constant term C of Eq. 1
     if constexpr (INJ) {  // after the update, before the store
       for (int f = 0; f < p.nfaults; ++f) {
         const LocalFault F = p.faults[f];
@@ -371,6 +407,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
         }
       }
     }
+    double* part = sPart + (it & 1) * (WARPS * TX);
     if constexpr (CHK) {
       double rs[RY], cs[V];
       if (full) partial_sums<T, true>(out, rs, cs, gyb, gx0, nx, ny);
@@ -378,28 +415,34 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 1)
       // b^s_y += sum over this tile's columns (Eq. 3)
       const double tot = row_reduce<RY>(rs, lane);
       const int gy = gyb + row_of_lane<RY>(lane);
-      #ifdef ABFT_EXP_NO_RED  // experiment builds only: partial sums without the L2 reductions
+#ifdef ABFT_EXP_NO_RED  // experiment builds only: partial sums without the L2 reductions
       if (final_lane<RY>(lane) && gy < ny && tot == -1.2345) Bg[gy] = tot;
 #else
       if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(z + 1) * ny + gy], tot);
 #endif
-      __syncthreads();  // the previous layer's column partials have been consumed
+      // column partials of this layer; double-buffered, so the one barrier per
+      // layer below also orders them against the reduction two layers later
+#ifndef ABFT_EXP_NO_COLSUM
 #pragma unroll
-      for (int k = 0; k < V; ++k) sPart[warp * TX + lane * V + k] = cs[k];
+      for (int k = 0; k < V; ++k) part[warp * TX + lane * V + k] = cs[k];
+#endif
     }
-    __syncthreads();  // every read of the lowest staged layer and of the source layer is done
+    __syncthreads();  // lowest staged layer consumed; this layer's column partials complete
     if (tid == 0) {
       fence_proxy_async();
       if (it + NS < nT) issue_T(it + NS);
-      if (hasP && it + NSP < nZ) issue_P(it + NSP);
     }
+#ifdef ABFT_EXP_NO_COLSUM
+    if constexpr (false) {
+#else
     if constexpr (CHK) {
+#endif
       // a^s_x += sum over this tile's rows (Eq. 2)
       if (tid < TX) {
-        double s = sPart[tid];
+        double s = part[tid];
 #pragma unroll
-        for (int w = 1; w < WARPS; ++w) s += sPart[w * TX + tid];
-        #ifdef ABFT_EXP_NO_RED
+        for (int w = 1; w < WARPS; ++w) s += part[w * TX + tid];
+#ifdef ABFT_EXP_NO_RED
         if (x0 + tid < nx && s == -1.2345) Ag[tid] = s;
 #else
         if (x0 + tid < nx) atomicAdd(&Ag[(size_t)(z + 1) * nx + x0 + tid], s);
