@@ -305,10 +305,14 @@ static int32_t check_layer(const or_problem* p, int64_t s, int64_t z, void* u,
                            or_record* recs, int64_t cap, int64_t* nrec, or_stats* st_) {
   const int64_t nx = p->nx, ny = p->ny;
   int64_t na = 0, nb = 0, x0 = -1, y0 = -1;
-  for (int64_t x = 0; x < nx; x++)
-    if (or_flag(PA[z * nx + x], A[z * nx + x], p->eps)) { if (x0 < 0) x0 = x; na++; }
   for (int64_t y = 0; y < ny; y++)
     if (or_flag(PB[z * ny + y], B[z * ny + y], p->eps)) { if (y0 < 0) y0 = y; nb++; }
+  /* "it is only necessary to perform the detection on one of the two
+     checksums.  If one or more errors are detected, only then ... interpolate
+     the other checksum and ... perform detection" (checksums == 1) */
+  if (p->checksums == 1 && nb == 0) return 0;
+  for (int64_t x = 0; x < nx; x++)
+    if (or_flag(PA[z * nx + x], A[z * nx + x], p->eps)) { if (x0 < 0) x0 = x; na++; }
   if (na == 0 && nb == 0) return 0;
   st_->detections++;
   or_record r;
@@ -389,6 +393,14 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
       or_sweep(p, cur, nxt, s, faults, nfaults);
       if (p->mode == OR_MODE_ONLINE) {
         or_checksums(p, nxt, An, Bn);                    /* step 1, fig.abft */
+        if (p->checksums == 1) {
+          /* a is not carried from sweep to sweep: a^{s-1} is the column sum
+             of u^{s-1} as it stands (computed only when needed;
+             its values enter only layers whose b flags, check_layer) */
+          double* Bt = malloc(sizeof(double) * nz * ny);
+          or_checksums(p, cur, Ap, Bt);
+          free(Bt);
+        }
         or_predict(p, Ap, Bp, cur, cA, cB, PA, PB);      /* step 2 */
         for (int64_t z = 0; z < nz; z++)                 /* step 3 + correction */
           if (check_layer(p, s, z, nxt, An, Bn, PA, PB, recs, cap, nrec, stats)) worst = 1;

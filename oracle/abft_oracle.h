@@ -54,7 +54,10 @@ typedef struct {
   const or_point* points;
   const or_source* sources;
   double eps;
-  int32_t mode, delta, correction_form, pad;
+  int32_t mode, delta, correction_form;
+  int32_t checksums;   /* online: 0 = a and b every sweep (SURVEY Q8 reading);
+                          1 = b every sweep, a only for layers whose b flags
+                          (the paper's recommendation) */
 } or_problem;
 
 /* flip bit `bit` of cell idx */

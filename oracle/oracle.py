@@ -54,7 +54,7 @@ class ProblemS(C.Structure):
                 ("npoints", C.c_int32), ("nsources", C.c_int32),
                 ("points", C.POINTER(Point)), ("sources", C.POINTER(Source)),
                 ("eps", C.c_double), ("mode", C.c_int32), ("delta", C.c_int32),
-                ("correction_form", C.c_int32), ("pad", C.c_int32)]
+                ("correction_form", C.c_int32), ("checksums", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -127,6 +127,7 @@ class OProblem:
         s.sources = C.cast(srcs, C.POINTER(Source))
         s.eps, s.mode, s.delta = prob.eps, prob.mode, prob.delta
         s.correction_form = prob.correction_form
+        s.checksums = getattr(prob, "checksums", 0)
         self.s = s
 
     @property

@@ -318,13 +318,15 @@ def _clean_states(p, op, u0, s):
     return O.run(oq, u0, s)["u"]
 
 
-def test_detection_closed_form_and_location_cfg1():
+@pytest.mark.parametrize("checksums", [0, 1])
+def test_detection_closed_form_and_location_cfg1(checksums):
     # For one flip at sweep s: delta = flipped - clean is exact; since the
     # prediction equals the clean checksum up to ~1e-8, the B (row) entry is
     # flagged iff |delta| > eps*|S + delta| (S clean row sum), same for A.
     # Every flip flagged in both vectors must be located at the injected cell
-    # and corrected (Eq. 8).
-    p = _cfg1_like()
+    # and corrected (Eq. 8).  checksums=1 (detect on b,
+    # compute and compare a only then): a record iff b is flagged.
+    p = _cfg1_like().replace(checksums=checksums)
     op = O.OProblem(p)
     u0 = field_u0(p).numpy()
     s = 10
@@ -345,7 +347,9 @@ def test_detection_closed_form_and_location_cfg1():
             continue                               # ambiguous band
         r = O.run(op, u0, s, [Fault(s, 0, y, x, bit)])
         expect_b, expect_a = mb > p.eps, ma > p.eps
-        if not (expect_a or expect_b):
+        if checksums == 1 and not expect_b:
+            assert r["records"] == []
+        elif not (expect_a or expect_b):
             assert r["records"] == []
         else:
             rec = r["records"][0]
@@ -359,6 +363,24 @@ def test_detection_closed_form_and_location_cfg1():
                 assert rec["vx"] != rec["vy"] or rec["corrected"] == np.float32(rec["vx"])
         checked += 1
     assert checked > 80
+
+
+def test_lazy_checksum_policy_equals_both_when_b_flags():
+    # P:271-273 / P:496-497: computing a only for layers whose b flags changes
+    # nothing when every flip is large enough to flag b (bits >= 24 of values
+    # in [323, 343) in 64-wide rows): same field bitwise, same records.
+    p = make_problem("cfg2", nx=64, ny=48, nz=5, sweeps=30)
+    u0 = field_u0(p).numpy()
+    P = field_power(p).numpy()
+    rng = random.Random(5)
+    faults = [Fault(s, rng.randrange(5), rng.randrange(48), rng.randrange(64), rng.randint(24, 30))
+              for s in range(3, 30, 4)]
+    r0 = O.run(O.OProblem(p, [P]), u0, p.sweeps, faults)
+    r1 = O.run(O.OProblem(p.replace(checksums=1), [P]), u0, p.sweeps, faults)
+    assert r0["stats"]["corrected"] == len(faults)
+    assert (r0["u"].view(np.uint32) == r1["u"].view(np.uint32)).all()
+    assert r0["records"] == r1["records"]
+    assert np.array_equal(r0["B"], r1["B"]) and np.array_equal(r0["A"], r1["A"])
 
 
 def test_paper_bits_0_12_undetected_high_bits_detected():
