@@ -70,6 +70,16 @@ typedef enum {
  * detect + correct every sweep (Section III), OFFLINE = detect every `delta`
  * sweeps + checkpoint rollback (Section IV). */
 typedef enum { ABFT_MODE_NONE = 0, ABFT_MODE_ONLINE = 1, ABFT_MODE_OFFLINE = 2 } abft_mode;
+/* Which actual checksum vectors an online step() computes.  BOTH: a and b of
+ * every layer every sweep, both compared.  LAZY: the paper's recommendation
+ * ("only one checksum vector is computed during the stencil sweep";
+ * P:496-497 "only necessary to perform the detection on one of the two
+ * checksums.  If one or more errors are detected, only then ... interpolate
+ * the other checksum"): b every sweep; for a layer whose b flags, a^{s-1} and
+ * a^s are computed from the fields and a' compared, to locate and correct.
+ * OFFLINE windows and the explicit sweep()/check()/correct() API always use
+ * BOTH. */
+typedef enum { ABFT_CK_BOTH = 0, ABFT_CK_LAZY = 1 } abft_checksum_policy;
 /* abft_record.status */
 typedef enum {
   ABFT_REC_CORRECTED = 1,     /* located by intersection, corrected (Eq. 8)      */
@@ -117,7 +127,7 @@ typedef struct {
   int32_t correction_form; /* 0: Eq. 8 with (a - u) re-summed over the other cells
                               (default); 1: literal fig.correction listing */
   int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
-  int32_t pad;
+  int32_t checksum_policy; /* abft_checksum_policy (ONLINE step() only) */
   const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by
                                  all ranks (one process per GPU, nranks > 1); NULL
                                  for nranks == 1 or for a local group member (see
@@ -211,7 +221,9 @@ int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b);
 int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected);
 
 /* Schedule bit-flips (test / measurement hook).  Replaces the pending list;
- * faults outside this rank's slab are ignored by this rank. */
+ * faults outside this rank's slab are ignored by this rank.  ABFT_EINVAL (and
+ * an empty list) if a fault is out of range, two faults hit the same cell in
+ * the same sweep, or more than 64 fall in this slab in one sweep. */
 int abft_stencil_set_faults(abft_stencil* h, const abft_fault* faults, int32_t n);
 
 /* Read-back.  All synchronise the handle's stream. */

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cstdlib>
 #include <vector>
 
@@ -102,9 +103,10 @@ struct Layout {
   int64_t px, plane;
   size_t field_bytes;
   // aux offsets
-  size_t off_gA[3], off_gB[3], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_st, off_src;
+  size_t off_gA[3], off_gB[3], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_lazy, off_st, off_src;
   size_t off_EX[3];  // x-edge ledger of each field buffer, [2][zc+2][ny] of dtype
   size_t aux_bytes;
+  size_t hot_bytes;  // prefix of aux touched every sweep
   bool pad_src;
 };
 
@@ -142,6 +144,7 @@ int validate(const abft_config* c) {
   if (c->mode < 0 || c->mode > 2) return ABFT_EINVAL;
   if (c->mode == ABFT_MODE_OFFLINE && c->delta < 1) return ABFT_EINVAL;
   if (c->correction_form != 0 && c->correction_form != 1) return ABFT_EINVAL;
+  if (c->checksum_policy != ABFT_CK_BOTH && c->checksum_policy != ABFT_CK_LAZY) return ABFT_EINVAL;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
   if (c->nranks > 1) {
     if ((c->rank == 0) != (c->z_begin == 0)) return ABFT_EINVAL;
@@ -163,13 +166,18 @@ Layout layout(const abft_config* c) {
   const size_t zc2 = (size_t)c->z_count + 2;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  // per-sweep vectors first (checksum generations, c_x / c_y, edge ledgers).
+  // A persisting-L2 window over them was measured: K2 unchanged, K1 2x slower
+  // (the carve-out starves the streaming sweep), so none is set.
   for (int g = 0; g < 3; ++g) { L.off_gA[g] = take(zc2 * c->nx * 8); L.off_gB[g] = take(zc2 * c->ny * 8); }
-  for (int g = 0; g < 2; ++g) { L.off_PA[g] = take(zc2 * c->nx * 8); L.off_PB[g] = take(zc2 * c->ny * 8); }
   L.off_cA = take((size_t)c->z_count * c->nx * 8);
   L.off_cB = take((size_t)c->z_count * c->ny * 8);
-  L.off_summ = take((size_t)c->z_count * sizeof(LayerSummary));
-  L.off_st = take(sizeof(DevState));
   for (int b = 0; b < 3; ++b) L.off_EX[b] = take((size_t)2 * zc2 * c->ny * L.esz);
+  L.off_summ = take((size_t)c->z_count * sizeof(LayerSummary));
+  L.off_lazy = take((size_t)c->z_count * sizeof(int));
+  L.off_st = take(sizeof(DevState));
+  L.hot_bytes = o;
+  for (int g = 0; g < 2; ++g) { L.off_PA[g] = take(zc2 * c->nx * 8); L.off_PB[g] = take(zc2 * c->ny * 8); }
   const int fs = field_source(c);
   L.pad_src = fs >= 0 && ((c->nx * L.esz) % 16 != 0 ||
                           (reinterpret_cast<uintptr_t>(c->sources[fs].field) % 16) != 0);
@@ -203,6 +211,7 @@ struct abft_stencil {
   double* PB[2];
   double *cA, *cB;
   LayerSummary* summ;
+  int* lazy_list;
   DevState* st;
   const void* src_field = nullptr;
   int64_t src_px = 0;
@@ -317,7 +326,7 @@ CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, c
 }
 
 // K1: step (1)
-int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk, int64_t sweep) {
+int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, int64_t sweep) {
   SweepParams p = h->sp;
   p.out = h->fb[dst];
   p.EX = h->cfg.mode != ABFT_MODE_NONE ? h->EX[dst] : nullptr;
@@ -342,8 +351,8 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, bool chk,
   cudaError_t e;
   if (h->ymarch)
     e = h->cfg.dtype == ABFT_F32
-            ? launch_k1y_f32(h->shape, chk, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p)
-            : launch_k1y_f64(h->shape, chk, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p);
+            ? launch_k1y_f32(h->shape, chk == K1_CK_AB, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p)
+            : launch_k1y_f64(h->shape, chk == K1_CK_AB, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p);
   else
     e = h->cfg.dtype == ABFT_F32
             ? launch_k1_f32(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], p)
@@ -364,6 +373,16 @@ int launch_check(abft_stencil* h, const CheckParams& p) {
   return ABFT_OK;
 }
 
+// K3 (lazy policy): a vectors + locate / correct of the layers K2 handed over
+int launch_lazy(abft_stencil* h, const CheckParams& p) {
+  cudaEvent_t* pe = prof_begin(h, 2);
+  cudaError_t e = launch_k3(h->cfg.dtype, h->shape, h->stream, p);
+  prof_end(h, pe);
+  h->launches++;
+  CK(e);
+  return ABFT_OK;
+}
+
 int launch_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
                  double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
                  int flags, int64_t sweep) {
@@ -373,7 +392,7 @@ int launch_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const d
 // a checked sweep: K1 (step (1)) then K2 (steps (2)-(5))
 int sweep_checked(abft_stencil* h, int src, int dst, double* A, double* B, const CheckParams& ck,
                   int64_t sweep) {
-  int r = launch_k1(h, src, dst, A, B, true, sweep);
+  int r = launch_k1(h, src, dst, A, B, K1_CK_AB, sweep);
   if (r) return r;
 #ifdef ABFT_EXP_NO_K2  // experiment builds only (tools/exp_build.py): K1 cost in isolation
   return ABFT_OK;
@@ -487,6 +506,17 @@ int online_sweep(Group& G) {
   const int gp = h0->gen, gn = (h0->gen + 1) % 3, gz = (h0->gen + 2) % 3;
   for (abft_stencil* h : G) {
     if (!h->next_zero) TRY(zero_gen(h, gn));
+    if (h->cfg.checksum_policy == ABFT_CK_LAZY) {
+      // b in the pass; a (generations used as scratch) by K3 only
+      // for layers whose b flagged
+      TRY(launch_k1(h, src, dst, nullptr, h->gB[gn], K1_CK_B, s));
+      CheckParams ck = make_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr,
+                                  nullptr, nullptr, h->gB[gz], CK_COMPARE | CK_CORRECT | CK_LAZY, s);
+      ck.Aw = h->gA[gp];
+      TRY(launch_check(h, ck));
+      TRY(launch_lazy(h, ck));
+      continue;
+    }
     TRY(sweep_checked(h, src, dst, h->gA[gn], h->gB[gn],
                       make_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr,
                                  nullptr, h->gA[gz], h->gB[gz], CK_COMPARE | CK_CORRECT, s),
@@ -508,7 +538,7 @@ int none_sweep(Group& G) {
   abft_stencil* h0 = G[0];
   const int64_t s = h0->sweeps + 1;
   const int src = h0->cur, dst = 1 - h0->cur;
-  for (abft_stencil* h : G) TRY(launch_k1(h, src, dst, nullptr, nullptr, false, s));
+  for (abft_stencil* h : G) TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
   TRY(halo_exchange(G, XSpec{dst, XV_NONE, 0}));
   for (abft_stencil* h : G) {
     h->prev = src;
@@ -564,7 +594,7 @@ int offline_window(Group& G, int L) {
         const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
         const double* pB = t == 1 ? h->gB[ckgen] : h->PB[(t - 1) & 1];
         if (!end) {
-          TRY(launch_k1(h, src, dst, nullptr, nullptr, false, s));
+          TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
           TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
                            nullptr, nullptr, CK_STORE_PRED, s));
         } else {
@@ -695,6 +725,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->cA = reinterpret_cast<double*>(h->aux + L.off_cA);
   h->cB = reinterpret_cast<double*>(h->aux + L.off_cB);
   h->summ = reinterpret_cast<LayerSummary*>(h->aux + L.off_summ);
+  h->lazy_list = reinterpret_cast<int*>(h->aux + L.off_lazy);
   for (int b = 0; b < 3; ++b) h->EX[b] = h->aux + L.off_EX[b];
   h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
   h->has_lo = cfg->rank > 0;
@@ -771,7 +802,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->ymarch = false;   // measured slower on cfg4 (profiles/r01): opt-in only
   if (const char* e = getenv("ABFT_K1_MARCH")) {
     if (e[0] == 'z') h->ymarch = false;
-    if (e[0] == 'y') h->ymarch = needs_z;
+    if (e[0] == 'y') h->ymarch = needs_z && cfg->checksum_policy == ABFT_CK_BOTH;
   }
   int ntx = 0, ntz = 0;
   if (h->ymarch) {
@@ -819,7 +850,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   memset(&cp, 0, sizeof(cp));
   cp.nx = (int)nx; cp.ny = (int)ny; cp.zc = (int)zc; cp.px = L.px; cp.plane = L.plane;
   cp.has_lo = h->has_lo; cp.has_hi = h->has_hi;
-  cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st;
+  cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st; cp.lazy_list = h->lazy_list;
   cp.npoints = cfg->npoints;
   for (int q = 0; q < cfg->npoints; ++q) {
     cp.di[q] = sp.di[q]; cp.dj[q] = sp.dj[q]; cp.dk[q] = sp.dk[q]; cp.w[q] = sp.w[q];
@@ -903,7 +934,7 @@ int abft_stencil_sweep(abft_stencil* h) {
   const int gn = (h->gen + 1) % 3;
   TRY(clear_summaries(h));
   TRY(zero_gen(h, gn));
-  TRY(launch_k1(h, src, dst, h->gA[gn], h->gB[gn], true, s));
+  TRY(launch_k1(h, src, dst, h->gA[gn], h->gB[gn], K1_CK_AB, s));
   TRY(halo_exchange(G, XSpec{dst, XV_GEN, gn}));
   h->prev = src;
   h->cur = dst;
@@ -960,6 +991,25 @@ int abft_stencil_set_faults(abft_stencil* h, const abft_fault* f, int32_t n) {
       return ABFT_EINVAL;
     h->faults.push_back(PendingFault{a, false});
   }
+  // one K1 launch carries a sweep's flips in its parameter block: at most
+  // kMaxFaultsPerLaunch per sweep in this slab, one per cell
+  std::vector<const abft_fault*> mine;
+  for (const PendingFault& pf : h->faults) {
+    const int64_t zl = pf.f.z - h->cfg.z_begin;
+    if (zl >= 0 && zl < h->cfg.z_count) mine.push_back(&pf.f);
+  }
+  std::sort(mine.begin(), mine.end(), [](const abft_fault* a, const abft_fault* b) {
+    return std::tie(a->sweep, a->z, a->y, a->x) < std::tie(b->sweep, b->z, b->y, b->x);
+  });
+  for (size_t i = 0, run = 1; i < mine.size(); ++i, ++run) {
+    if (i > 0 && mine[i]->sweep != mine[i - 1]->sweep) run = 1;
+    const bool same_cell = i > 0 && mine[i]->sweep == mine[i - 1]->sweep && mine[i]->z == mine[i - 1]->z &&
+                           mine[i]->y == mine[i - 1]->y && mine[i]->x == mine[i - 1]->x;
+    if (same_cell || run > (size_t)kMaxFaultsPerLaunch) {
+      h->faults.clear();
+      return ABFT_EINVAL;
+    }
+  }
   return ABFT_OK;
 }
 
@@ -983,15 +1033,24 @@ int abft_stencil_read_field(abft_stencil* h, void* dst) {
 int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
   if (!h || !A || !B) return ABFT_EINVAL;
   const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
-  int g = h->gen;
+  int g = h->gen, ga = h->gen;
   if (h->cfg.mode == ABFT_MODE_NONE) {  // no running checksums: compute them now (Eqs. 2-3)
-    g = (h->gen + 1) % 3;
+    g = ga = (h->gen + 1) % 3;
     if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,
                         h->gA[g], h->gB[g], 1, h->stream) != cudaSuccess)
       return ABFT_ECUDA;
     h->launches += 2;
+  } else if (h->cfg.mode == ABFT_MODE_ONLINE && h->cfg.checksum_policy == ABFT_CK_LAZY &&
+             !h->pending_check) {
+    // lazy policy: a is not carried; compute it now into generation gen + 2
+    // (cleared again by the next sweep's K2 before it is accumulated into)
+    ga = (h->gen + 2) % 3;
+    if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,
+                        h->gA[ga], h->gB[ga], 1, h->stream) != cudaSuccess)
+      return ABFT_ECUDA;
+    h->launches += 2;
   }
-  CK(cudaMemcpyAsync(A, h->gA[g] + nx, sizeof(double) * nx * zc, cudaMemcpyDefault, h->stream));
+  CK(cudaMemcpyAsync(A, h->gA[ga] + nx, sizeof(double) * nx * zc, cudaMemcpyDefault, h->stream));
   CK(cudaMemcpyAsync(B, h->gB[g] + ny, sizeof(double) * ny * zc, cudaMemcpyDefault, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return ABFT_OK;

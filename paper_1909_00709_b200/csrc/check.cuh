@@ -44,7 +44,7 @@ __device__ __forceinline__ void bump(DevState* st, int k, long long v = 1) {
   atomicAdd(reinterpret_cast<unsigned long long*>(&st->cnt[k]), (unsigned long long)v);
 }
 
-constexpr int kCheckThreads = 256;
+constexpr int kCheckThreads = 128;   // 10+ CTAs per SM: every layer of a 1024-layer slab in one wave
 
 // one entry of a'_x (A == true) or b'_y of layer z, Theorem 1 (Eqs. 4-5):
 //   a'_x = c_x + sum_S w (a_{zeta(z+k)}[x+i] + alpha_{x+i, j})
@@ -183,10 +183,43 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
 // layer's flags meet in shared memory, so the same CTA then locates, corrects
 // and records (Eq. 8, fig.correction) -- no cross-CTA handshake.
 constexpr int kCheckUnroll = 4;
+
+// one vector (a' over x if A, else b' over y) of layer z: predict, store the
+// prediction (offline P / explicit check), compare with the actual checksum,
+// clear the generation of sweep s + 2; flags meet in shared memory.
+template <typename T, int S, bool A>
+__device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n, int* s_k, double* s_pred) {
+  const int n = A ? p.nx : p.ny, bz = z + 1;
+  const double* act = A ? p.Ac : p.Bc;
+  double* pout = A ? p.PAo : p.PBo;
+  double* zero = A ? p.zA : p.zB;
+  const bool cmp = p.flags & CK_COMPARE;
+  for (int e0 = threadIdx.x; e0 < n; e0 += kCheckThreads * kCheckUnroll) {
+    double pr[kCheckUnroll], ac[kCheckUnroll];
+#pragma unroll
+    for (int u = 0; u < kCheckUnroll; ++u) {
+      const int e = e0 + u * kCheckThreads;
+      const bool in = e < n;
+      pr[u] = in ? predict_entry<T, S, A>(p, z, e) : 0.0;
+      ac[u] = (in && cmp) ? act[(size_t)bz * n + e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kCheckUnroll; ++u) {
+      const int e = e0 + u * kCheckThreads;
+      if (e >= n) break;
+      if (p.flags & CK_STORE_PRED) pout[(size_t)bz * n + e] = pr[u];
+      if (cmp && flag_rel(pr[u], ac[u], p.eps)) {
+        atomicAdd(s_n, 1);
+        atomicMax(s_k, 0x7fffffff - e);
+        *s_pred = pr[u];
+      }
+      if (zero) zero[(size_t)bz * n + e] = 0.0;
+    }
+  }
+}
 template <typename T, int S>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
   const int z = blockIdx.x, bz = z + 1;
-  const int nx = p.nx, ny = p.ny, ne = nx + ny;
   const int tid = threadIdx.x;
   LayerSummary* L = &p.summ[z];
   __shared__ int s_na, s_nb, s_xk, s_yk;
@@ -197,41 +230,22 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   if (!(p.flags & CK_FROM_SUMMARY)) {
     if (tid == 0) { s_na = 0; s_nb = 0; s_xk = 0; s_yk = 0; s_pa = 0.0; s_pb = 0.0; }
     __syncthreads();
-    for (int e0 = 0; e0 < ne; e0 += kCheckThreads * kCheckUnroll) {
-      double pr[kCheckUnroll];
-#pragma unroll
-      for (int u = 0; u < kCheckUnroll; ++u) {
-        const int e = e0 + u * kCheckThreads + tid;
-        pr[u] = 0.0;
-        if (e < nx) pr[u] = predict_entry<T, S, true>(p, z, e);
-        else if (e < ne) pr[u] = predict_entry<T, S, false>(p, z, e - nx);
-      }
-#pragma unroll
-      for (int u = 0; u < kCheckUnroll; ++u) {
-        const int e = e0 + u * kCheckThreads + tid;
-        if (e < nx) {
-          if (p.flags & CK_STORE_PRED) p.PAo[(size_t)bz * nx + e] = pr[u];
-          if ((p.flags & CK_COMPARE) && flag_rel(pr[u], p.Ac[(size_t)bz * nx + e], p.eps)) {
-            atomicAdd(&s_na, 1);
-            atomicMax(&s_xk, 0x7fffffff - e);
-            s_pa = pr[u];
-          }
-          if (p.zA) p.zA[(size_t)bz * nx + e] = 0.0;   // generation of sweep s + 2
-        } else if (e < ne) {
-          const int y = e - nx;
-          if (p.flags & CK_STORE_PRED) p.PBo[(size_t)bz * ny + y] = pr[u];
-          if ((p.flags & CK_COMPARE) && flag_rel(pr[u], p.Bc[(size_t)bz * ny + y], p.eps)) {
-            atomicAdd(&s_nb, 1);
-            atomicMax(&s_yk, 0x7fffffff - y);
-            s_pb = pr[u];
-          }
-          if (p.zB) p.zB[(size_t)bz * ny + y] = 0.0;
-        }
-      }
-    }
+    // a' (entries x) then b' (entries y): no divergent entry kinds inside a
+    // round, so the loads of all kCheckUnroll entries are in flight together.
+    // Lazy policy: b' only; a is computed by K3 for the
+    // layers whose b flags.
+    if (!(p.flags & CK_LAZY)) check_vec<T, S, true>(p, z, &s_na, &s_xk, &s_pa);
+    check_vec<T, S, false>(p, z, &s_nb, &s_yk, &s_pb);
     if (!(p.flags & CK_COMPARE)) return;
     __syncthreads();
     na = s_na; nb = s_nb; xk = s_xk; yk = s_yk; pa = s_pa; pb = s_pb;
+    if (p.flags & CK_LAZY) {      // hand the flagged layer to K3
+      if (nb && tid == 0) {
+        L->nb = nb; L->yk = yk; L->pb = pb; L->cnt = 0;
+        p.lazy_list[atomicAdd(&p.st->lazy_n, 1)] = z;
+      }
+      return;
+    }
     if (p.flags & CK_SUMMARY) {   // explicit check(): keep the summary for correct()
       if (tid == 0) {
         L->na = na; L->nb = nb; L->xk = xk; L->yk = yk; L->pa = pa; L->pb = pb;
@@ -248,6 +262,81 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   const int x0 = na ? 0x7fffffff - xk : -1;
   const int y0 = nb ? 0x7fffffff - yk : -1;
   finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
+}
+
+// K3 (lazy checksum policy): for every layer z whose b flagged in K2, the
+// second checksum vector "only in case of error, to enable correction"
+// (P:271-273): a^{s-1} of the layers the prediction reads
+// (zeta(z-1), z, zeta(z+1), column sums of u^{s-1}, halo layers included) and
+// a^s of z (column sums of u^s), each column summed sequentially in
+// ascending y like Eq. 2; then the CTA that completes the layer predicts a'
+// (Theorem 1), compares, locates and corrects as K2 does for policy BOTH.
+// grid (ceil(nx / kCheckThreads), 4 vector kinds, slot stride); exits at once
+// when no layer flagged.  The last CTA of the grid resets the layer list.
+template <typename T>
+__device__ __forceinline__ double col_sum(const T* col, int64_t px, int ny) {
+  double s = 0.0;
+  int y = 0;
+  for (; y + 8 <= ny; y += 8) {
+    T v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = col[(size_t)(y + j) * px];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += (double)v[j];
+  }
+  for (; y < ny; ++y) s += (double)col[(size_t)y * px];
+  return s;
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__ CheckParams p) {
+  __shared__ int s_na, s_xk, s_last;
+  __shared__ double s_pa;
+  __shared__ double red[kCheckThreads / 32];
+  const int tid = threadIdx.x, nx = p.nx, ny = p.ny, zc = p.zc;
+  const int n = *(volatile int*)&p.st->lazy_n;
+  const int kind = blockIdx.y;   // 0, 1, 2: a^{s-1} of zeta(z-1), z, zeta(z+1); 3: a^s of z
+  const int x = blockIdx.x * kCheckThreads + tid;
+  for (int i = blockIdx.z; i < n; i += gridDim.z) {
+    const int z = p.lazy_list[i];
+    LayerSummary* L = &p.summ[z];
+    const int bl = kind == 3 ? z + 1 : zmap(z + kind - 1, zc, p.has_lo, p.has_hi);
+    const T* u = reinterpret_cast<const T*>(kind == 3 ? p.ucur : p.uprev);
+    double* dst = (kind == 3 ? p.Ac : p.Aw) + (size_t)bl * nx;
+    if (x < nx) dst[x] = col_sum<T>(u + (size_t)bl * p.plane + x, p.px, ny);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(&L->cnt, 1) == 4 * (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (tid == 0) { s_na = 0; s_xk = 0; s_pa = 0.0; }
+      __syncthreads();
+      CheckParams q = p;
+      q.flags = CK_COMPARE;
+      q.Ap = p.Aw;
+      q.PAo = nullptr;
+      q.zA = nullptr;
+      check_vec<T, S, true>(q, z, &s_na, &s_xk, &s_pa);
+      __syncthreads();
+      const int na = s_na, nb = L->nb;
+      const int x0 = na ? 0x7fffffff - s_xk : -1, y0 = 0x7fffffff - L->yk;
+      const double pa = s_pa, pb = L->pb;
+      __syncthreads();
+      if (tid == 0) { L->nb = 0; L->yk = 0; L->cnt = 0; }
+      finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&p.st->lazy_done, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
+      p.st->lazy_n = 0;
+      p.st->lazy_done = 0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K0

@@ -13,7 +13,7 @@ namespace abft {
 
 constexpr int kMaxPoints = 27;   // radius-1 stencils in 3D
 constexpr int kMaxSources = 4;
-constexpr int kMaxFaultsPerLaunch = 16;
+constexpr int kMaxFaultsPerLaunch = 64;   // scheduled flips per sweep and slab (set_faults checks)
 constexpr int kRecordCap = 4096;
 
 // ------------------------------------------------------------------ shapes
@@ -80,6 +80,9 @@ template <int S> struct SwapYZ {
   }
 };
 
+// which actual checksums K1 accumulates in its pass
+enum K1Checksums { K1_CK_NONE = 0, K1_CK_AB = 1 /* a and b */, K1_CK_B = 2 /* b only (lazy a) */ };
+
 // ------------------------------------------------------------ param blocks
 struct LocalFault { int z, y, x, bit; };  // slab-local layer, row, column
 
@@ -93,6 +96,8 @@ struct DevState {
   int dirty;               // offline: flagged layers in the last window check
   long long flag_a, flag_b;  // explicit check(): flagged entries
   long long ncorr;           // explicit correct(): corrections
+  int lazy_n;                // lazy checksum policy: layers whose b flagged this sweep
+  int lazy_done;             // K3 CTAs finished (the last one resets lazy_n)
   abft_record rec[kRecordCap];
 };
 enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCORR,
@@ -103,7 +108,7 @@ enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCO
 struct LayerSummary {
   int na, nb;      // flagged entries of a (over x) and b (over y)
   int xk, yk;      // max of (INT_MAX - index) over flagged entries: the first flagged index
-  int spare;
+  int cnt;         // lazy policy: K3 CTAs done with this layer's a vectors
   int pad;
   double pa, pb;   // predicted a'_{x0}, b'_{y0} (meaningful when na == 1 / nb == 1)
 };
@@ -116,6 +121,7 @@ enum CheckFlags {
   CK_PERSIST = 16,       // second attempt of a window
   CK_SUMMARY = 32,       // write LayerSummary (explicit check())
   CK_FROM_SUMMARY = 64,  // correct() from a stored summary, no prediction
+  CK_LAZY = 128,         // checksum policy LAZY: compare b only; flagged layers -> K3
 };
 
 struct CheckParams {
@@ -138,6 +144,8 @@ struct CheckParams {
   void* EXc;           // edge columns of ucur (patched by a correction)
   LayerSummary* summ;  // [zc]
   DevState* st;
+  double* Aw;          // lazy policy: a^{s-1} written by K3 (the predictor input generation)
+  int* lazy_list;      // lazy policy: flagged layers of this sweep, [zc]
   int npoints;
   int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
   double w[kMaxPoints];

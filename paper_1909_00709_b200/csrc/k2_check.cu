@@ -33,6 +33,24 @@ cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckP
   return dtype == ABFT_F32 ? k2_go<float>(shape, g, s, p) : k2_go<double>(shape, g, s, p);
 }
 
+template <typename T>
+static cudaError_t k3_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
+  switch (shape) {
+    case SHAPE_FIG2_5PT: k3_lazy<T, SHAPE_FIG2_5PT><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7:
+    case SHAPE_HOTSPOT7_FS: k3_lazy<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_BOX27: k3_lazy<T, SHAPE_BOX27><<<g, kCheckThreads, 0, s>>>(p); break;
+    default: k3_lazy<T, SHAPE_GENERIC><<<g, kCheckThreads, 0, s>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p) {
+  // x-tiles x 4 vector kinds x 4 concurrent flagged layers (more loop)
+  const dim3 g((p.nx + kCheckThreads - 1) / kCheckThreads, 4, 4);
+  return dtype == ABFT_F32 ? k3_go<float>(shape, g, s, p) : k3_go<double>(shape, g, s, p);
+}
+
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s) {
   FieldVal f{u, px, plane, dtype};

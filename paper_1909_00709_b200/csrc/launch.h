@@ -13,9 +13,9 @@ K1Geometry k1_geometry(int dtype);
 // y-march (3D shapes): tile_x x tile_y = x-columns x z-layers of one tile
 K1Geometry k1y_geometry(int dtype);
 
-cudaError_t launch_k1_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
+cudaError_t launch_k1_f32(int shape, int chk, bool inj, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
-cudaError_t launch_k1_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
+cudaError_t launch_k1_f64(int shape, int chk, bool inj, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
 cudaError_t launch_k1y_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
                            const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
@@ -25,6 +25,8 @@ cudaError_t launch_k1y_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_
 int k1y_occ_f32(int shape);
 int k1y_occ_f64(int shape);
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
+// K3 (lazy checksum policy)
+cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p);
 // K0: A[z + off][x] / B[z + off][y] sums of the field buffer `u`
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s);

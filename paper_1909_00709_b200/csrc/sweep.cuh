@@ -118,6 +118,22 @@ __device__ __forceinline__ void partial_sums(const T (&out)[Tile<T>::RY][Tile<T>
   }
 }
 
+// rows-only variant (checksum policy LAZY: b every sweep)
+template <typename T, bool FULL, int RY>
+__device__ __forceinline__ void row_sums(const T (&out)[RY][16 / sizeof(T)], double (&rs)[RY],
+                                         int gyb, int gx0, int nx, int ny) {
+  constexpr int V = 16 / (int)sizeof(T);
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double d = (double)out[r][k];
+      if (!FULL) d = (gyb + r < ny && gx0 + k < nx) ? d : 0.0;
+      rs[r] = k == 0 ? d : rs[r] + d;
+    }
+  }
+}
+
 // One layer of one thread: RY x V outputs of Eq. 1 from the staged planes
 // pl[0..2] (offset -1, 0, +1 along the march axis), the canonical FMA chain in
 // the shape's point order; srow[t] = staged row of input row (first - 1 + t),
@@ -231,10 +247,11 @@ __device__ __forceinline__ void add_sources(T (&out)[RY][16 / sizeof(T)], const 
   }
 }
 
-// K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: accumulate the
-// actual checksums.  INJ: apply this launch's scheduled bit-flips.
+// K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: which actual
+// checksums the pass accumulates (K1_CK_*).  INJ: apply this launch's
+// scheduled bit-flips.
 // grid (x-tiles, y-tiles, z-chunks); each CTA marches up its z-chunk.
-template <typename T, int S, bool CHK, bool INJ>
+template <typename T, int S, int CHK, bool INJ>
 __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
     k1_sweep(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ SweepParams p) {
   using TL = Tile<T>;
@@ -408,45 +425,38 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
       }
     }
     double* part = sPart + (it & 1) * (WARPS * TX);
-    if constexpr (CHK) {
+    if constexpr (CHK != K1_CK_NONE) {
       double rs[RY], cs[V];
-      if (full) partial_sums<T, true>(out, rs, cs, gyb, gx0, nx, ny);
-      else partial_sums<T, false>(out, rs, cs, gyb, gx0, nx, ny);
+      if constexpr (CHK == K1_CK_AB) {
+        if (full) partial_sums<T, true>(out, rs, cs, gyb, gx0, nx, ny);
+        else partial_sums<T, false>(out, rs, cs, gyb, gx0, nx, ny);
+      } else {
+        if (full) row_sums<T, true>(out, rs, gyb, gx0, nx, ny);
+        else row_sums<T, false>(out, rs, gyb, gx0, nx, ny);
+      }
       // b^s_y += sum over this tile's columns (Eq. 3)
       const double tot = row_reduce<RY>(rs, lane);
       const int gy = gyb + row_of_lane<RY>(lane);
-#ifdef ABFT_EXP_NO_RED  // experiment builds only: partial sums without the L2 reductions
-      if (final_lane<RY>(lane) && gy < ny && tot == -1.2345) Bg[gy] = tot;
-#else
       if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(z + 1) * ny + gy], tot);
-#endif
-      // column partials of this layer; double-buffered, so the one barrier per
-      // layer below also orders them against the reduction two layers later
-#ifndef ABFT_EXP_NO_COLSUM
+      if constexpr (CHK == K1_CK_AB) {
+        // column partials of this layer; double-buffered, so the one barrier per
+        // layer below also orders them against the reduction two layers later
 #pragma unroll
-      for (int k = 0; k < V; ++k) part[warp * TX + lane * V + k] = cs[k];
-#endif
+        for (int k = 0; k < V; ++k) part[warp * TX + lane * V + k] = cs[k];
+      }
     }
     __syncthreads();  // lowest staged layer consumed; this layer's column partials complete
     if (tid == 0) {
       fence_proxy_async();
       if (it + NS < nT) issue_T(it + NS);
     }
-#ifdef ABFT_EXP_NO_COLSUM
-    if constexpr (false) {
-#else
-    if constexpr (CHK) {
-#endif
+    if constexpr (CHK == K1_CK_AB) {
       // a^s_x += sum over this tile's rows (Eq. 2)
       if (tid < TX) {
         double s = part[tid];
 #pragma unroll
         for (int w = 1; w < WARPS; ++w) s += part[w * TX + tid];
-#ifdef ABFT_EXP_NO_RED
-        if (x0 + tid < nx && s == -1.2345) Ag[tid] = s;
-#else
         if (x0 + tid < nx) atomicAdd(&Ag[(size_t)(z + 1) * nx + x0 + tid], s);
-#endif
       }
     }
   }

@@ -262,3 +262,75 @@ def test_ymarch_segments_and_tile_edges(nx, ny, nz, march):
     faults = [Fault(2 + i, z, (7 * i) % ny, (37 * i + 127) % nx, 30 - i) for i, z in enumerate(zs)]
     faults += [Fault(9, nz // 2, ny - 1, nx - 1, 29), Fault(12, nz // 3, 0, 128 % nx, 28)]
     parity(p, faults=faults)
+
+
+# ---- checksum policy LAZY: b every sweep, a on detection
+
+@pytest.mark.parametrize("seed", range(0, 8))
+def test_lazy_cfg1_seeds(seed):
+    parity(make_problem("cfg1", seed=seed, checksums=1))
+
+
+def test_lazy_cfg2_full_online_10_flips():
+    g, o = parity(make_problem("cfg2", checksums=1))
+    assert o["stats"]["corrected"] >= 1
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(203, 77, 9), (129, 33, 3), (5, 3, 4), (1, 1, 1), (260, 1, 2)])
+def test_lazy_hotspot_ragged_shapes(nx, ny, nz):
+    p = make_problem("cfg2", nx=nx, ny=ny, nz=nz, sweeps=25, nfaults=2, checksums=1)
+    faults = [Fault(7, nz - 1, ny - 1, nx - 1, 30), Fault(15, 0, 0, 0, 27), Fault(15, nz // 2, ny // 2, nx // 2, 28)]
+    faults = list({(f.sweep, f.z, f.y, f.x): f for f in faults}.values())   # one flip per cell and sweep
+    parity(p, faults=faults)
+
+
+def test_lazy_many_flagged_layers_in_one_sweep():
+    # more flagged layers than K3's concurrent slots: every one is handled
+    p = make_problem("cfg3", nx=96, ny=64, nz=20, sweeps=6, nfaults=0, checksums=1)
+    faults = [Fault(3, z, (5 * z) % 64, (11 * z) % 96, 29) for z in range(20)]
+    faults += [Fault(5, z, 0, 95, 30) for z in range(0, 20, 3)]
+    g, o = parity(p, faults=faults)
+    assert o["stats"]["corrected"] >= 20
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_lazy_generic_stencil(dtype):
+    rng = random.Random(7)
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+    rng.shuffle(offs)
+    w = [rng.uniform(0.01, 1.0) for _ in range(9)]
+    pts = [(a, b, c, v / sum(w)) for (a, b, c), v in zip(offs[:9], w)]
+    p = Problem("gen", 150, 61, 6, dtype, pts, [(0.002, True, 0.0)],
+                eps=1e-5 if dtype == "f32" else 1e-10, mode=1, sweeps=12, init=(1.0, 2.0),
+                power=(0.0, 1.0), checksums=1)
+    faults = [Fault(3, 2, 30, 70, 30 if dtype == "f32" else 62), Fault(9, 5, 60, 149, 27)]
+    parity(p, faults=faults)
+
+
+def test_lazy_cfg5_reduced_fp64_box27_online():
+    parity(make_problem("cfg5", nx=66, ny=40, nz=7, sweeps=15, nfaults=5, mode=1, checksums=1))
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_lazy_slab_group_equals_oracle(G):
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=1, checksums=1)
+    faults = fault_schedule(p) + [Fault(9, 5, 3, 4, 30), Fault(9, 6, 70, 90, 29), Fault(11, 4, 0, 0, 30)]
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, G, faults)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+    assert np.array_equal(g["A"], o["A"]) and np.array_equal(g["B"], o["B"])
+
+
+def test_set_faults_rejects_duplicates_and_overfull_sweeps():
+    from paper_1909_00709_b200 import abft
+    p = make_problem("cfg2", nx=64, ny=64, nz=80, sweeps=2)
+    dev = torch.device("cuda:0")
+    st = abft.from_problem(p, field_u0(p, dev), field_power(p, dev), device=dev)
+    with pytest.raises(abft.AbftError):
+        st.set_faults([Fault(1, 3, 4, 5, 20), Fault(1, 3, 4, 5, 21)])
+    with pytest.raises(abft.AbftError):
+        st.set_faults([Fault(1, z, 0, 0, 20) for z in range(65)])
+    st.set_faults([Fault(1, z, 0, 0, 20) for z in range(64)] + [Fault(2, 0, 0, 0, 20)])
+    st.destroy()

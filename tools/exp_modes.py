@@ -14,8 +14,9 @@ p = make_problem(cfg)
 dev = torch.device("cuda:0")
 u0, P = field_u0(p, dev), field_power(p, dev)
 res = {"lib": name}
-for mode, tag in ((0, "unprot"), (1, "prot"), (0, "unprot2"), (1, "prot2")):
-    st = abft.from_problem(p, u0, P, device=dev, mode=mode)
+for mode, tag, pol in ((0, "unprot", 0), (1, "prot", 0), (1, "lazy", 1), (0, "unprot2", 0),
+                       (1, "prot2", 0), (1, "lazy2", 1)):
+    st = abft.from_problem(p, u0, P, device=dev, mode=mode, checksum_policy=pol)
     st.step(5)
     torch.cuda.synchronize()
     f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
