@@ -40,6 +40,7 @@ os.environ.setdefault("OMP_NUM_THREADS", str(_CORES))
 import torch  # noqa: E402
 
 from abft_inputs import fault_schedule, field_power, field_u0, make_problem  # noqa: E402
+from paper_1909_00709_b200 import dist as D  # noqa: E402
 
 METRIC = "protected GCell-updates/s at 1/2/4/8 B200, %HBM roofline, ABFT overhead %"
 UNIT = "GCell-updates/s"
@@ -141,21 +142,11 @@ def timed(stream, fn):
 
 
 def max_over_ranks(v: float, world: int) -> float:
-    if world == 1:
-        return v
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return D.max_over_ranks(v, world, device="cuda")
 
 
 def sum_over_ranks(v: float, world: int) -> float:
-    if world == 1:
-        return v
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return D.sum_over_ranks(v, world, device="cuda")
 
 
 def barrier(world):
@@ -188,10 +179,7 @@ def run_ours(a):
     p = make_problem(a.config)
     if not a.strong:            # weak scaling: each rank owns a slab of the config's size
         p = p.replace(nz=p.nz * world)
-    if p.nz % world:
-        raise SystemExit(f"nz={p.nz} not divisible by {world} ranks")
-    zc = p.nz // world
-    z0 = rank * zc
+    z0, zc = D.slab(p.nz, world, rank)
     pol = abft.ABFT_CK_LAZY if a.policy == "lazy" else abft.ABFT_CK_BOTH
     pol_other = abft.ABFT_CK_BOTH if pol == abft.ABFT_CK_LAZY else abft.ABFT_CK_LAZY
     cells_local = p.nx * p.ny * zc

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
     if (p.flags & CK_LAZY) {      // hand the flagged layer to K3
       if (nb && tid == 0) {
         L->nb = nb; L->yk = yk; L->pb = pb; L->cnt = 0;
-        p.lazy_list[atomicAdd(&p.st->lazy_n, 1)] = z;
+        p.lazy_list[atomicAdd(&p.st->lazy_n[p.sweep & 1], 1)] = z;
       }
       return;
     }
@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
 // ascending y like Eq. 2; then the CTA that completes the layer predicts a'
 // (Theorem 1), compares, locates and corrects as K2 does for policy BOTH.
 // grid (ceil(nx / kCheckThreads), 4 vector kinds, slot stride); exits at once
-// when no layer flagged.  The last CTA of the grid resets the layer list.
+// when no layer flagged.  Layer lists alternate by sweep parity: K3 of sweep s
+// clears the count of sweep s + 1 before K2 of s + 1 appends to it.
 template <typename T>
 __device__ __forceinline__ double col_sum(const T* col, int64_t px, int ny) {
   double s = 0.0;
@@ -294,7 +295,10 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
   __shared__ double s_pa;
   __shared__ double red[kCheckThreads / 32];
   const int tid = threadIdx.x, nx = p.nx, ny = p.ny, zc = p.zc;
-  const int n = *(volatile int*)&p.st->lazy_n;
+  const int n = *(volatile int*)&p.st->lazy_n[p.sweep & 1];
+  // the next sweep's K2 counts into the other slot: clear it (nobody reads it now)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
+    p.st->lazy_n[(p.sweep + 1) & 1] = 0;
   const int kind = blockIdx.y;   // 0, 1, 2: a^{s-1} of zeta(z-1), z, zeta(z+1); 3: a^s of z
   const int x = blockIdx.x * kCheckThreads + tid;
   for (int i = blockIdx.z; i < n; i += gridDim.z) {
@@ -329,13 +333,6 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
       finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
     }
     __syncthreads();
-  }
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(&p.st->lazy_done, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
-      p.st->lazy_n = 0;
-      p.st->lazy_done = 0;
-    }
   }
 }
 

@@ -96,8 +96,7 @@ struct DevState {
   int dirty;               // offline: flagged layers in the last window check
   long long flag_a, flag_b;  // explicit check(): flagged entries
   long long ncorr;           // explicit correct(): corrections
-  int lazy_n;                // lazy checksum policy: layers whose b flagged this sweep
-  int lazy_done;             // K3 CTAs finished (the last one resets lazy_n)
+  int lazy_n[2];             // lazy checksum policy: layers whose b flagged, by sweep parity
   abft_record rec[kRecordCap];
 };
 enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCORR,

@@ -1,0 +1,84 @@
+"""Host-side logic of the z-slab decomposition: which layers a
+rank owns, which layers and checksum rows cross each slab face after a sweep,
+and the reductions bench.py uses for max-over-ranks timing.  No numerics: the
+halo itself moves inside libabft_stencil.so (NCCL send/recv over NVLink,
+`exchange_nccl`, or device copies for a local group); this module states the
+same plan so it can be checked on CPU with the gloo backend.
+
+Buffer-layer convention of the library (include/abft_stencil.h):
+a slab of zc layers lives in buffer layers 1..zc; layer 0 and zc+1 hold the
+neighbours' boundary layers (the halo), or nothing at a global domain face
+(the clamp of P:289-292 reuses layer 1 / zc there).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Tuple
+
+
+def slab(nz: int, world: int, rank: int) -> Tuple[int, int]:
+    """(z_begin, z_count) of `rank`: contiguous, the first nz % world ranks get
+    one layer more.  Every rank owns >= 1 layer (requires nz >= world)."""
+    if not (0 <= rank < world) or nz < world:
+        raise ValueError(f"cannot split {nz} layers over {world} ranks")
+    base, extra = divmod(nz, world)
+    z0 = rank * base + min(rank, extra)
+    return z0, base + (1 if rank < extra else 0)
+
+
+def weak_nz(nz_per_rank: int, world: int) -> int:
+    """Global layer count of a weak-scaling run: every rank owns nz_per_rank."""
+    return nz_per_rank * world
+
+
+def neighbours(rank: int, world: int) -> Tuple[Optional[int], Optional[int]]:
+    """(lower, upper) neighbour rank in z, None at a global face."""
+    return (rank - 1 if rank > 0 else None, rank + 1 if rank + 1 < world else None)
+
+
+def halo_plan(rank: int, world: int, zc: int) -> List[Tuple[int, int, int]]:
+    """(peer, send_layer, recv_layer) per face, in buffer layers: the boundary
+    layer goes to the neighbour, whose boundary layer lands in the halo slot.
+    The checksum rows a[layer], b[layer] (or the offline prediction rows) of the
+    same layers travel with them.  Lower face first -- the order the library
+    posts its sends / receives inside one NCCL group."""
+    lo, hi = neighbours(rank, world)
+    plan = []
+    if lo is not None:
+        plan.append((lo, 1, 0))
+    if hi is not None:
+        plan.append((hi, zc, zc + 1))
+    return plan
+
+
+def exchange(rank: int, plan, send_fn, recv_fn) -> None:
+    """Run a halo plan with point-to-point callables that may block: on every
+    face the lower rank sends first and the upper rank receives first, faces in
+    plan order (lower face first), so a chain of blocking pairs cannot deadlock."""
+    for peer, s_layer, r_layer in plan:
+        if rank < peer:
+            send_fn(peer, s_layer)
+            recv_fn(peer, r_layer)
+        else:
+            recv_fn(peer, r_layer)
+            send_fn(peer, s_layer)
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a per-rank value (bench timing: the slowest rank defines the step)."""
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, world: int, device=None) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
