@@ -182,7 +182,10 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
 // KU entries of a' and b' per round with all their loads in flight; the
 // layer's flags meet in shared memory, so the same CTA then locates, corrects
 // and records (Eq. 8, fig.correction) -- no cross-CTA handshake.
-constexpr int kCheckUnroll = 4;
+#ifndef ABFT_KU
+#define ABFT_KU 4
+#endif
+constexpr int kCheckUnroll = ABFT_KU;
 
 // one vector (a' over x if A, else b' over y) of layer z: predict, store the
 // prediction (offline P / explicit check), compare with the actual checksum,

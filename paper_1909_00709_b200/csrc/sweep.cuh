@@ -42,6 +42,7 @@ template <typename T> struct Tile {
 #ifndef ABFT_NS
 #define ABFT_NS 4
 #endif
+
   static constexpr int RY = sizeof(T) == 4 ? ABFT_RY_F32 : 2;  // output rows per thread
   static constexpr int TY = WARPS * RY;
   static constexpr int ROWS = TY + 2;
@@ -252,7 +253,10 @@ __device__ __forceinline__ void add_sources(T (&out)[RY][16 / sizeof(T)], const 
 // scheduled bit-flips.
 // grid (x-tiles, y-tiles, z-chunks); each CTA marches up its z-chunk.
 template <typename T, int S, int CHK, bool INJ>
-__global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
+#ifndef ABFT_K1_MINB
+#define ABFT_K1_MINB 2
+#endif
+__global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABFT_K1_MINB)
     k1_sweep(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ SweepParams p) {
   using TL = Tile<T>;
   constexpr int V = TL::V, TX = TL::TX, HV = TL::HV, HX = TL::HX, RY = TL::RY, TY = TL::TY;
@@ -315,10 +319,12 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
   }
   T c0 = T(0), c1 = T(0), s1 = T(0);
   if constexpr (FS) { c0 = pcoef<T>(p, 0); c1 = pcoef<T>(p, 1); s1 = pscal<T>(p, 1); }
-  T pv[RY][V], pn[RY][V];
-  if (hasP) load_src<T, RY>(pn, p, zs, gyb, gx0, full);
+  // source-field registers of two consecutive layers, ping-ponged by the
+  // 2-way unrolled layer loop below (no register copies per layer)
+  T pa[RY][V], pb[RY][V];
+  if (hasP) load_src<T, RY>(pa, p, zs, gyb, gx0, full);
 
-  for (int z = zs; z < ze; ++z) {
+  auto layer = [&](const int z, T (&pv)[RY][V], T (&pn)[RY][V]) {
     const int it = z - zs;
     const T* pl[3];
     if (NZ) {
@@ -334,13 +340,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
       mbar_wait(&barT[it % NS], (it / NS) & 1);
       pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
     }
-    if (hasP) {
-#pragma unroll
-      for (int r = 0; r < RY; ++r)
-#pragma unroll
-        for (int k = 0; k < V; ++k) pv[r][k] = pn[r][k];
-      if (z + 1 < ze) load_src<T, RY>(pn, p, z + 1, gyb, gx0, full);
-    }
+    if (hasP && z + 1 < ze) load_src<T, RY>(pn, p, z + 1, gyb, gx0, full);
 
     T out[RY][V];
     if constexpr (!GEN) {
@@ -445,10 +445,12 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
         for (int k = 0; k < V; ++k) part[warp * TX + lane * V + k] = cs[k];
       }
     }
-    __syncthreads();  // lowest staged layer consumed; this layer's column partials complete
-    if (tid == 0) {
-      fence_proxy_async();
-      if (it + NS < nT) issue_T(it + NS);
+    {
+      __syncthreads();  // lowest staged layer consumed; this layer's column partials complete
+      if (tid == 0) {
+        fence_proxy_async();
+        if (it + NS < nT) issue_T(it + NS);
+      }
     }
     if constexpr (CHK == K1_CK_AB) {
       // a^s_x += sum over this tile's rows (Eq. 2)
@@ -459,7 +461,13 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * 2)
         if (x0 + tid < nx) atomicAdd(&Ag[(size_t)(z + 1) * nx + x0 + tid], s);
       }
     }
+  };
+  int z = zs;
+  for (; z + 1 < ze; z += 2) {
+    layer(z, pa, pb);
+    layer(z + 1, pb, pa);
   }
+  if (z < ze) layer(z, pa, pb);
 }
 
 }  // namespace abft
