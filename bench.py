@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--strong", action="store_true",
                     help="split the config's domain over the ranks (default: weak scaling, "
                          "every rank owns a slab of the config's size)")
+    ap.add_argument("--nz-per-gpu", type=int, default=0,
+                    help="weak scaling: layers per rank (0 = the config's nz; cfg5: 128, its "
+                         "per-GPU slab at G=8)")
     ap.add_argument("--policy", default="lazy", choices=["lazy", "both"],
                     help="checksum policy of the headline run (the other is measured too)")
     a = ap.parse_args()
@@ -161,6 +164,14 @@ def shift(faults, k):
     return [Fault(f.sweep + k, f.z, f.y, f.x, f.bit) for f in faults]
 
 
+def stencil_name(p) -> str:
+    if len(p.points) == 7 and p.sources:
+        return "HotSpot3D 7-point"
+    if len(p.points) == 27:
+        return "27-point box"
+    return f"{len(p.points)}-point"
+
+
 # ----------------------------------------------------------------- ours
 def run_ours(a):
     from paper_1909_00709_b200 import abft
@@ -178,7 +189,9 @@ def run_ours(a):
         nccl_id = obj[0]
     p = make_problem(a.config)
     if not a.strong:            # weak scaling: each rank owns a slab of the config's size
-        p = p.replace(nz=p.nz * world)
+        per = a.nz_per_gpu or (128 if a.config == "cfg5" else p.nz)
+        p = p.replace(nz=per * world)
+    pmode = p.mode              # online (cfg1-4) or offline (cfg5: period 5)
     z0, zc = D.slab(p.nz, world, rank)
     pol = abft.ABFT_CK_LAZY if a.policy == "lazy" else abft.ABFT_CK_BOTH
     pol_other = abft.ABFT_CK_BOTH if pol == abft.ABFT_CK_LAZY else abft.ABFT_CK_LAZY
@@ -216,16 +229,16 @@ def run_ours(a):
         return out
 
     with torch.cuda.stream(stream):
-        rA = protected_run(abft.ABFT_MODE_ONLINE, True)               # headline: flips on
-        rE = protected_run(abft.ABFT_MODE_ONLINE, True, policy=pol_other)
+        rA = protected_run(pmode, True)               # headline: flips on
+        rE = protected_run(pmode, True, policy=pol_other)
         # overhead (t_protected / t_unprotected - 1, error-free runs): the
         # three error-free runs interleaved, 3 rounds, median of each (clocks
         # drift under the power cap; interleaving exposes every run to it alike)
         reps = {"B": [], "C": [], "D": []}
         for _ in range(3):
             reps["C"].append(protected_run(abft.ABFT_MODE_NONE, False, prof=True))      # unprotected
-            reps["B"].append(protected_run(abft.ABFT_MODE_ONLINE, False, prof=True))    # protected
-            reps["D"].append(protected_run(abft.ABFT_MODE_ONLINE, False, prof=True, policy=pol_other))
+            reps["B"].append(protected_run(pmode, False, prof=True))    # protected
+            reps["D"].append(protected_run(pmode, False, prof=True, policy=pol_other))
         rB, rC, rD = (sorted(reps[k], key=lambda r: r["ms"])[1] for k in ("B", "C", "D"))
     ck = clocks.stop()
     tA = max_over_ranks(rA["ms"], world)
@@ -252,7 +265,9 @@ def run_ours(a):
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            if tj.get("config") == a.config and tj.get("policy", "lazy") == a.policy:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     launches = sum_over_ranks(rA["launches"], world)
@@ -301,10 +316,11 @@ def run_ours(a):
             "vs_baseline": None,
             "dtype": "f32" if p.dtype == "f32" else "f64",
             "data": "synthetic (seeded splitmix64; Rodinia HotSpot3D inputs not available)",
-            "config": {"workload": f"{a.config}: HotSpot3D 7-point {p.nx}x{p.ny}x{p.nz} "
-                                   f"{p.dtype}, online ABFT, {K} sweeps, "
-                                   f"{len(faults)} scheduled bit-flips",
-                       "checksum_policy": ("lazy: b every sweep, a for layers whose b flags "
+            "config": {"workload": f"{a.config}: {stencil_name(p)} {p.nx}x{p.ny}x{p.nz} "
+                                   f"{p.dtype}, {'online' if pmode == 1 else 'offline (period %d)' % p.delta}"
+                                   f" ABFT, {K} sweeps, {len(faults)} scheduled bit-flips",
+                       "checksum_policy": ("offline windows: a and b at each window end" if pmode == 2 else
+                                           "lazy: b every sweep, a for layers whose b flags "
                                            "(PAPER.md:271-273, 496-497)") if pol == abft.ABFT_CK_LAZY
                        else "both: a and b every sweep in the K1 pass",
                        "nx": p.nx, "ny": p.ny, "nz": p.nz, "z_per_gpu": zc,
@@ -325,8 +341,10 @@ def run_ours(a):
             "hbm_roofline_frac_step": round(value * 1e9 * bytes_cell / (peak * 1e9) / world, 4),
             "roofline": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(k1_gbs / peak, 4), "traffic": traffic,
-                         "kernel": "k1_sweep<float,HOTSPOT7_FS,%s,INJ=0> (protected)" % (
-                             "K1_CK_B" if pol == abft.ABFT_CK_LAZY else "K1_CK_AB"),
+                         "kernel": ("k1_sweep<%s,%s,%s,INJ=0> (protected)" % (
+                             "float" if p.dtype == "f32" else "double", stencil_name(p),
+                             "K1_CK_B" if pol == abft.ABFT_CK_LAZY else "K1_CK_AB")) if pmode == 1
+                         else "k1_sweep (offline: K1_CK_NONE within a window, K1_CK_AB at its end)",
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "algorithmic_bytes_per_launch": bytes_cell * cells_local,
                          "k1_ms": round(k1_ms, 5), "k1_unprotected_ms": round(k1_ms_unprot, 5),
