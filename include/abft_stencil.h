@@ -115,7 +115,8 @@ typedef struct {
   int64_t z_begin;      /* first global layer of this rank's slab */
   int64_t z_count;      /* layers owned by this rank, >= 1 */
   int32_t dtype;        /* abft_dtype */
-  int32_t bc;           /* abft_bc; this build implements ABFT_BC_CLAMP */
+  int32_t bc;           /* abft_bc: all four; PERIODIC needs nranks == 1 (else
+                           ABFT_EUNSUPPORTED) and always runs the z-march K1 */
   double bc_value;      /* ghost value for ABFT_BC_CONSTANT */
   int32_t npoints;      /* 1 .. 27 */
   int32_t nsources;     /* 0 .. 4 */

@@ -40,7 +40,10 @@ def flags() -> list:
 
 
 def _sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    # heaviest translation units first (the K1 instantiations), so the
+    # parallel build's critical path is as short as possible
+    srcs = glob.glob(os.path.join(CSRC, "*.cu"))
+    return sorted(srcs, key=lambda f: (not os.path.basename(f).startswith("k1"), f))
 
 
 def _deps():
@@ -62,8 +65,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     fl = flags()
 
+    shared = [d for d in _deps() if not d.endswith(".cu")]
+    newest_shared = max(os.path.getmtime(d) for d in shared)
+
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and \
+                os.path.getmtime(obj) >= max(newest_shared, os.path.getmtime(src)):
+            return obj   # incremental: source and every shared header older than the object
         cmd = [NVCC] + fl + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

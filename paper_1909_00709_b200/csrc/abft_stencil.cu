@@ -152,7 +152,10 @@ int validate(const abft_config* c) {
   } else if (c->z_begin != 0 || c->z_count != c->nz_global) {
     return ABFT_EINVAL;
   }
-  if (c->bc != ABFT_BC_CLAMP) return ABFT_EUNSUPPORTED;  // periodic / zero / constant: SURVEY NEXT-2
+  if (c->bc == ABFT_BC_CONSTANT && !isfinite(c->bc_value)) return ABFT_EINVAL;
+  // periodic wraps z across the whole domain: one slab only (a ring exchange
+  // between the first and last rank is not implemented)
+  if (c->bc == ABFT_BC_PERIODIC && c->nranks > 1) return ABFT_EUNSUPPORTED;
   return ABFT_OK;
 }
 
@@ -329,6 +332,7 @@ CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, c
 int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, int64_t sweep) {
   SweepParams p = h->sp;
   p.out = h->fb[dst];
+  p.uin = h->fb[src];
   p.EX = h->cfg.mode != ABFT_MODE_NONE ? h->EX[dst] : nullptr;
   p.A = A;
   p.B = B;
@@ -802,7 +806,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->ymarch = false;   // measured slower on cfg4 (profiles/r01): opt-in only
   if (const char* e = getenv("ABFT_K1_MARCH")) {
     if (e[0] == 'z') h->ymarch = false;
-    if (e[0] == 'y') h->ymarch = needs_z && cfg->checksum_policy == ABFT_CK_BOTH;
+    if (e[0] == 'y') h->ymarch = needs_z && cfg->checksum_policy == ABFT_CK_BOTH && cfg->bc == ABFT_BC_CLAMP;
   }
   int ntx = 0, ntz = 0;
   if (h->ymarch) {
@@ -830,6 +834,8 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   memset(&sp, 0, sizeof(sp));
   sp.nx = (int)nx; sp.ny = (int)ny; sp.zc = (int)zc; sp.zchunk = h->zchunk;
   sp.ntx = ntx; sp.ntz = ntz;
+  sp.bc = cfg->bc;
+  sp.g = cfg->bc == ABFT_BC_CONSTANT ? rnd(cfg->dtype, cfg->bc_value) : 0.0;
   sp.src = h->src_field;
   sp.spx = h->src_px;
   sp.splane = h->src_px * ny;
@@ -850,6 +856,8 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   memset(&cp, 0, sizeof(cp));
   cp.nx = (int)nx; cp.ny = (int)ny; cp.zc = (int)zc; cp.px = L.px; cp.plane = L.plane;
   cp.has_lo = h->has_lo; cp.has_hi = h->has_hi;
+  cp.bc = cfg->bc;
+  cp.g = sp.g;
   cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st; cp.lazy_list = h->lazy_list;
   cp.npoints = cfg->npoints;
   for (int q = 0; q < cfg->npoints; ++q) {
@@ -858,6 +866,18 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   cp.eps = cfg->epsilon;
   cp.form = cfg->correction_form;
   cp.z_begin = cfg->z_begin;
+
+  // constant ghosts: the halo layers no neighbour owns are the
+  // ghost layers of z (zmap); zero ghosts are the init memset
+  if (cfg->bc == ABFT_BC_CONSTANT) {
+    for (int b = 0; b < h->nbuf; ++b) {
+      if (!h->has_lo && launch_fill(cfg->dtype, h->fb[b], L.plane, sp.g, h->stream) != cudaSuccess)
+        return fail(ABFT_ECUDA);
+      if (!h->has_hi && launch_fill(cfg->dtype, h->fb[b] + (size_t)(zc + 1) * L.plane * esz, L.plane, sp.g,
+                                    h->stream) != cudaSuccess)
+        return fail(ABFT_ECUDA);
+    }
+  }
 
   // K0: trusted a^0, b^0 of u0 and the pre-computed c_x, c_y
   if (launch_k0_field(cfg->dtype, h->fb[0], L.px, L.plane, (int)nx, (int)ny, (int)zc, h->gA[0], h->gB[0],

@@ -66,18 +66,37 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
     int di, dj, dk;
     if constexpr (GEN) { di = p.di[q]; dj = p.dj[q]; dk = p.dk[q]; }
     else { di = Shape<S>::off(q, 0); dj = Shape<S>::off(q, 1); dk = Shape<S>::off(q, 2); }
-    const int zq = zmap(z + dk, zc, p.has_lo, p.has_hi);
+    const int bc = p.bc;
+    const bool ghostv = bc == ABFT_BC_ZERO || bc == ABFT_BC_CONSTANT;
+    const double g = bc == ABFT_BC_CONSTANT ? p.g : 0.0;
+    const int zq = zmap(z + dk, zc, p.has_lo, p.has_hi, bc);
+    const bool zg = zghost(z + dk, zc, p.has_lo, p.has_hi, bc);
     if (A) {
-      const int xr = max(0, min(e + di, nx - 1));
+      const int xs = e + di;
+      const bool xg = ghostv && (xs < 0 || xs >= nx);
+      if (zg || xg) {          // the shifted column lies in the ghost region
+        Sv[q] = __dmul_rn((double)ny, g);
+        continue;
+      }
+      const int xr = (xs >= 0 && xs < nx) ? xs : (bc == ABFT_BC_PERIODIC ? wrap(xs, nx) : max(0, min(xs, nx - 1)));
       double s = p.Ap[(size_t)zq * nx + xr];
-      if (dj != 0) {   // alpha at the shifted column (Q3): ghost row minus the far edge row (clamp)
+      if (dj != 0) {   // alpha at the shifted column (Q3): ghost row minus the far edge row
         const T* col = up + (size_t)zq * p.plane + xr;
         const double top = (double)col[0], bot = (double)col[(size_t)(ny - 1) * p.px];
-        s = __dadd_rn(s, dj < 0 ? __dsub_rn(top, bot) : __dsub_rn(bot, top));
+        // value of row -1 / row ny: clamp top / bot, periodic bot / top, zero 0, constant g
+        const double gt = bc == ABFT_BC_CLAMP ? top : (bc == ABFT_BC_PERIODIC ? bot : g);
+        const double gb = bc == ABFT_BC_CLAMP ? bot : (bc == ABFT_BC_PERIODIC ? top : g);
+        s = __dadd_rn(s, dj < 0 ? __dsub_rn(gt, bot) : __dsub_rn(gb, top));
       }
       Sv[q] = s;
     } else {
-      const int yr = max(0, min(e + dj, ny - 1));
+      const int ys = e + dj;
+      const bool yg = ghostv && (ys < 0 || ys >= ny);
+      if (zg || yg) {
+        Sv[q] = __dmul_rn((double)nx, g);
+        continue;
+      }
+      const int yr = (ys >= 0 && ys < ny) ? ys : (bc == ABFT_BC_PERIODIC ? wrap(ys, ny) : max(0, min(ys, ny - 1)));
       double s = p.Bp[(size_t)zq * ny + yr];
       if (di != 0) {   // beta: the x-edge columns of u^{s-1} (ledger, or the halo layer itself)
         double lft, rgt;
@@ -89,7 +108,9 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
           lft = (double)row[0];
           rgt = (double)row[nx - 1];
         }
-        s = __dadd_rn(s, di < 0 ? __dsub_rn(lft, rgt) : __dsub_rn(rgt, lft));
+        const double gl = bc == ABFT_BC_CLAMP ? lft : (bc == ABFT_BC_PERIODIC ? rgt : g);
+        const double gr = bc == ABFT_BC_CLAMP ? rgt : (bc == ABFT_BC_PERIODIC ? lft : g);
+        s = __dadd_rn(s, di < 0 ? __dsub_rn(gl, rgt) : __dsub_rn(gr, lft));
       }
       Sv[q] = s;
     }
@@ -191,57 +212,83 @@ constexpr int kCheckUnroll = ABFT_KU;
 // prediction (offline P / explicit check), compare with the actual checksum,
 // clear the generation of sweep s + 2; flags meet in shared memory.
 template <typename T, int S, bool A>
-__device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n, int* s_k, double* s_pred) {
-  const int n = A ? p.nx : p.ny, bz = z + 1;
+__device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n, int* s_k, double* s_pred,
+                                          int part = 0, int nparts = 1) {
+  const int nn = A ? p.nx : p.ny, bz = z + 1;
+  const int lo = (int)((int64_t)nn * part / nparts), n = (int)((int64_t)nn * (part + 1) / nparts);
   const double* act = A ? p.Ac : p.Bc;
   double* pout = A ? p.PAo : p.PBo;
   double* zero = A ? p.zA : p.zB;
   const bool cmp = p.flags & CK_COMPARE;
-  for (int e0 = threadIdx.x; e0 < n; e0 += kCheckThreads * kCheckUnroll) {
+  for (int e0 = lo + threadIdx.x; e0 < n; e0 += kCheckThreads * kCheckUnroll) {
     double pr[kCheckUnroll], ac[kCheckUnroll];
 #pragma unroll
     for (int u = 0; u < kCheckUnroll; ++u) {
       const int e = e0 + u * kCheckThreads;
       const bool in = e < n;
       pr[u] = in ? predict_entry<T, S, A>(p, z, e) : 0.0;
-      ac[u] = (in && cmp) ? act[(size_t)bz * n + e] : 0.0;
+      ac[u] = (in && cmp) ? act[(size_t)bz * nn + e] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kCheckUnroll; ++u) {
       const int e = e0 + u * kCheckThreads;
       if (e >= n) break;
-      if (p.flags & CK_STORE_PRED) pout[(size_t)bz * n + e] = pr[u];
+      if (p.flags & CK_STORE_PRED) pout[(size_t)bz * nn + e] = pr[u];
       if (cmp && flag_rel(pr[u], ac[u], p.eps)) {
         atomicAdd(s_n, 1);
         atomicMax(s_k, 0x7fffffff - e);
         *s_pred = pr[u];
       }
-      if (zero) zero[(size_t)bz * n + e] = 0.0;
+      if (zero) zero[(size_t)bz * nn + e] = 0.0;
     }
   }
 }
 template <typename T, int S>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
   const int z = blockIdx.x, bz = z + 1;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, part = blockIdx.y, nparts = gridDim.y;
   LayerSummary* L = &p.summ[z];
-  __shared__ int s_na, s_nb, s_xk, s_yk;
+  __shared__ int s_na, s_nb, s_xk, s_yk, s_last;
   __shared__ double s_pa, s_pb;
   __shared__ double red[kCheckThreads / 32];
   int na, nb, xk, yk;
   double pa, pb;
+  (void)bz;
   if (!(p.flags & CK_FROM_SUMMARY)) {
     if (tid == 0) { s_na = 0; s_nb = 0; s_xk = 0; s_yk = 0; s_pa = 0.0; s_pb = 0.0; }
     __syncthreads();
     // a' (entries x) then b' (entries y): no divergent entry kinds inside a
     // round, so the loads of all kCheckUnroll entries are in flight together.
     // Lazy policy: b' only; a is computed by K3 for the
-    // layers whose b flags.
-    if (!(p.flags & CK_LAZY)) check_vec<T, S, true>(p, z, &s_na, &s_xk, &s_pa);
-    check_vec<T, S, false>(p, z, &s_nb, &s_yk, &s_pb);
+    // layers whose b flags.  nparts > 1 (few layers): this CTA's share.
+    if (!(p.flags & CK_LAZY)) check_vec<T, S, true>(p, z, &s_na, &s_xk, &s_pa, part, nparts);
+    check_vec<T, S, false>(p, z, &s_nb, &s_yk, &s_pb, part, nparts);
     if (!(p.flags & CK_COMPARE)) return;
     __syncthreads();
-    na = s_na; nb = s_nb; xk = s_xk; yk = s_yk; pa = s_pa; pb = s_pb;
+    if (nparts > 1) {
+      // merge this share into the layer summary; the CTA that completes the
+      // layer continues with the layer's totals
+      if (tid == 0) {
+        if (s_na) { atomicAdd(&L->na, s_na); atomicMax(&L->xk, s_xk); L->pa = s_pa; }
+        if (s_nb) { atomicAdd(&L->nb, s_nb); atomicMax(&L->yk, s_yk); L->pb = s_pb; }
+        __threadfence();
+        s_last = atomicAdd(&L->cnt2, 1) == nparts - 1;
+      }
+      __syncthreads();
+      if (!s_last) return;
+      __threadfence();
+      na = *(volatile int*)&L->na; nb = *(volatile int*)&L->nb;
+      xk = *(volatile int*)&L->xk; yk = *(volatile int*)&L->yk;
+      pa = *(volatile double*)&L->pa; pb = *(volatile double*)&L->pb;
+      __syncthreads();
+      if (tid == 0) {
+        L->cnt2 = 0;
+        if (!(p.flags & (CK_LAZY | CK_SUMMARY))) { L->na = 0; L->nb = 0; L->xk = 0; L->yk = 0; }
+        if (p.flags & CK_LAZY) { L->na = 0; L->xk = 0; }
+      }
+    } else {
+      na = s_na; nb = s_nb; xk = s_xk; yk = s_yk; pa = s_pa; pb = s_pb;
+    }
     if (p.flags & CK_LAZY) {      // hand the flagged layer to K3
       if (nb && tid == 0) {
         L->nb = nb; L->yk = yk; L->pb = pb; L->cnt = 0;
@@ -307,7 +354,7 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
   for (int i = blockIdx.z; i < n; i += gridDim.z) {
     const int z = p.lazy_list[i];
     LayerSummary* L = &p.summ[z];
-    const int bl = kind == 3 ? z + 1 : zmap(z + kind - 1, zc, p.has_lo, p.has_hi);
+    const int bl = kind == 3 ? z + 1 : zmap(z + kind - 1, zc, p.has_lo, p.has_hi, p.bc);
     const T* u = reinterpret_cast<const T*>(kind == 3 ? p.ucur : p.uprev);
     double* dst = (kind == 3 ? p.Ac : p.Aw) + (size_t)bl * nx;
     if (x < nx) dst[x] = col_sum<T>(u + (size_t)bl * p.plane + x, p.px, ny);

@@ -108,7 +108,7 @@ struct LayerSummary {
   int na, nb;      // flagged entries of a (over x) and b (over y)
   int xk, yk;      // max of (INT_MAX - index) over flagged entries: the first flagged index
   int cnt;         // lazy policy: K3 CTAs done with this layer's a vectors
-  int pad;
+  int cnt2;        // K2 CTAs of this layer done (split layers, gridDim.y > 1)
   double pa, pb;   // predicted a'_{x0}, b'_{y0} (meaningful when na == 1 / nb == 1)
 };
 
@@ -127,6 +127,8 @@ struct CheckParams {
   int nx, ny, zc;
   int64_t px, plane;
   int has_lo, has_hi;
+  int bc;              // abft_bc
+  double g;            // ghost value (ABFT_BC_CONSTANT), rounded to the dtype
   const void* uprev;   // field buffer read by the sweep (ledger for alpha / beta)
   void* ucur;          // field buffer written by the sweep (corrected in place)
   const double* Ap;    // predictor input a^{s-1} (or offline P^{s-1}), [(zc+2)][nx]
@@ -159,6 +161,9 @@ struct SweepParams {
   int64_t px;          // row pitch of the field buffers (elements)
   int64_t plane;       // layer pitch = px * ny
   int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)
+  int bc;              // abft_bc of Eq. 1's ghosts
+  double g;            // ghost value (ABFT_BC_CONSTANT), rounded to the dtype
+  const void* uin;     // input field buffer (periodic wrap reads at tile edges)
   void* out;           // output field buffer (layer 0 = lower halo)
   double* A;           // checksum generation accumulated by this sweep, [(zc+2)][nx]
   double* B;           // [(zc+2)][ny]
@@ -250,10 +255,24 @@ __device__ __forceinline__ double flip_bit(double v, int bit) {
 // buffer layer index of slab-local layer q in [-1, zc] (layer 0 = lower halo):
 // interior q -> q + 1; beyond a neighbour -> its halo layer; beyond the global
 // domain edge -> clamp (P:289-292 bounce-back extended to z).
-__host__ __device__ __forceinline__ int zmap(int q, int zc, int has_lo, int has_hi) {
-  if (q < 0) return has_lo ? 0 : 1;
-  if (q >= zc) return has_hi ? zc + 1 : zc;
+// Zero / constant ghosts: the buffer layers 0 / zc+1 that no
+// neighbour owns are filled with the ghost value at init, so they are the
+// ghost layer.  Periodic (single slab): wrap.
+__host__ __device__ __forceinline__ int zmap(int q, int zc, int has_lo, int has_hi, int bc = ABFT_BC_CLAMP) {
+  if (q < 0) {
+    if (has_lo) return 0;
+    return bc == ABFT_BC_CLAMP ? 1 : (bc == ABFT_BC_PERIODIC ? zc : 0);
+  }
+  if (q >= zc) {
+    if (has_hi) return zc + 1;
+    return bc == ABFT_BC_CLAMP ? zc : (bc == ABFT_BC_PERIODIC ? 1 : zc + 1);
+  }
   return q + 1;
 }
+// global layer index q beyond a global face with zero / constant ghosts?
+__host__ __device__ __forceinline__ bool zghost(int q, int zc, int has_lo, int has_hi, int bc) {
+  return (bc == ABFT_BC_ZERO || bc == ABFT_BC_CONSTANT) && ((q < 0 && !has_lo) || (q >= zc && !has_hi));
+}
+__host__ __device__ __forceinline__ int wrap(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }
 
 }  // namespace abft

@@ -1,0 +1,5 @@
+// z-march K1 for float fields, shape SHAPE_HOTSPOT7 (see sweep.cuh, k1_shape.inc).
+#define K1_T float
+#define K1_S SHAPE_HOTSPOT7
+#define K1_FN launch_k1_f32_s2
+#include "k1_shape.inc"

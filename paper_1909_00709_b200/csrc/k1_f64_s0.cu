@@ -1,0 +1,5 @@
+// z-march K1 for double fields, shape SHAPE_GENERIC (see sweep.cuh, k1_shape.inc).
+#define K1_T double
+#define K1_S SHAPE_GENERIC
+#define K1_FN launch_k1_f64_s0
+#include "k1_shape.inc"

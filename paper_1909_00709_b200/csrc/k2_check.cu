@@ -1,4 +1,6 @@
 // K2 / K0 instantiations (see check.cuh).
+#include <algorithm>
+
 #include "check.cuh"
 #include "launch.h"
 #include "sweep.cuh"
@@ -29,7 +31,21 @@ static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
 }
 
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p) {
-  const dim3 g(zc);
+  // one CTA per layer; few layers (cfg1-3 tiles): split each layer's entries
+  // over up to 2 x SMs / zc CTAs, at least kCheckThreads entries each
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
+  }
+  int parts = 1;
+  if (!(p.flags & CK_FROM_SUMMARY)) {
+    const int want = (2 * nsm + zc - 1) / zc;
+    const int cap = (std::max(p.nx, p.ny) + kCheckThreads - 1) / kCheckThreads;
+    parts = std::max(1, std::min(want, cap));
+  }
+  const dim3 g(zc, parts);
   return dtype == ABFT_F32 ? k2_go<float>(shape, g, s, p) : k2_go<double>(shape, g, s, p);
 }
 
@@ -49,6 +65,19 @@ cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p
   // x-tiles x 4 vector kinds x 4 concurrent flagged layers (more loop)
   const dim3 g((p.nx + kCheckThreads - 1) / kCheckThreads, 4, 4);
   return dtype == ABFT_F32 ? k3_go<float>(shape, g, s, p) : k3_go<double>(shape, g, s, p);
+}
+
+template <typename T>
+__global__ void fill_value(T* p, int64_t n, T v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>(1184, (n + 255) / 256);
+  if (dtype == ABFT_F32) fill_value<float><<<blocks, 256, 0, s>>>(static_cast<float*>(ptr), n, (float)v);
+  else fill_value<double><<<blocks, 256, 0, s>>>(static_cast<double*>(ptr), n, v);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,

@@ -17,6 +17,14 @@ cudaError_t launch_k1_f32(int shape, int chk, bool inj, dim3 grid, cudaStream_t 
                           const CUtensorMap& tu, const SweepParams& p);
 cudaError_t launch_k1_f64(int shape, int chk, bool inj, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
+// per (dtype, shape) translation units (k1_<dtype>_s<shape>.cu)
+#define ABFT_K1_DECL(name) \
+  cudaError_t name(int chk, bool inj, dim3 grid, cudaStream_t s, const CUtensorMap& tu, const SweepParams& p);
+ABFT_K1_DECL(launch_k1_f32_s0) ABFT_K1_DECL(launch_k1_f32_s1) ABFT_K1_DECL(launch_k1_f32_s2)
+ABFT_K1_DECL(launch_k1_f32_s3) ABFT_K1_DECL(launch_k1_f32_s4)
+ABFT_K1_DECL(launch_k1_f64_s0) ABFT_K1_DECL(launch_k1_f64_s1) ABFT_K1_DECL(launch_k1_f64_s2)
+ABFT_K1_DECL(launch_k1_f64_s3) ABFT_K1_DECL(launch_k1_f64_s4)
+#undef ABFT_K1_DECL
 cudaError_t launch_k1y_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
                            const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
 cudaError_t launch_k1y_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
@@ -25,6 +33,8 @@ cudaError_t launch_k1y_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_
 int k1y_occ_f32(int shape);
 int k1y_occ_f64(int shape);
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
+// fill n elements of a field buffer with v (constant ghost layers)
+cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t s);
 // K3 (lazy checksum policy)
 cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p);
 // K0: A[z + off][x] / B[z + off][y] sums of the field buffer `u`

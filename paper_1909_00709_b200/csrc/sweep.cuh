@@ -142,10 +142,21 @@ __device__ __forceinline__ void row_sums(const T (&out)[RY][16 / sizeof(T)], dou
 // x = 0 or x = nx - 1, so out-of-domain x reads take the clamped value.
 // SH is the shape seen in the staged coordinates (Shape<S>, or SwapYZ<S> for
 // the y-march): off(q, 2) selects the plane, off(q, 1) the row.
+// What an edge tile needs to build the ghosts of Eq. 1 (P:289-292 clamp,
+// P:413-415 periodic / zero / constant): BC, ghost value, the input planes in
+// global memory (periodic wrap reads), the row pitch and the thread's rows.
+template <typename T> struct EdgeCtx {
+  int bc;
+  T g;
+  const T* up[3];
+  int64_t px;
+  int gyb, ny;
+};
+
 template <typename T, class SH, int RY, bool NZ, bool EDGE>
 __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
                                               const int (&srow)[RY + 2], const T (&wr)[SH::NP],
-                                              int lane, int gx0, int nx) {
+                                              int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
   constexpr int V = 16 / (int)sizeof(T), TX = 32 * V, HV = V, NP = SH::NP;
   T W[3][RY + 2][V + 2];
   // lanes 0 / 31 need the staged halo element left / right of the tile: every
@@ -176,10 +187,32 @@ __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], cons
         W[d][t][0] = left;
         W[d][t][V + 1] = right;
         if constexpr (EDGE) {
-          if (gx0 == 0) W[d][t][0] = W[d][t][1];
+          if (ec.bc == ABFT_BC_CLAMP) {
+            if (gx0 == 0) W[d][t][0] = W[d][t][1];
 #pragma unroll
-          for (int c2 = 1; c2 < V + 2; ++c2)
-            if (gx0 - 1 + c2 >= nx) W[d][t][c2] = W[d][t][c2 - 1];
+            for (int c2 = 1; c2 < V + 2; ++c2)
+              if (gx0 - 1 + c2 >= nx) W[d][t][c2] = W[d][t][c2 - 1];
+          }
+        }
+      }
+      if constexpr (EDGE) {
+        // constant / periodic ghosts (zero ghosts are the TMA's zero fill of
+        // out-of-range boxes): every out-of-domain entry of this row
+        if (ec.bc == ABFT_BC_CONSTANT || ec.bc == ABFT_BC_PERIODIC) {
+          const int gy = ec.gyb - 1 + t;
+          const bool yo = gy < 0 || gy >= ec.ny;
+#pragma unroll
+          for (int c2 = 0; c2 < V + 2; ++c2) {
+            const int gx = gx0 - 1 + c2;
+            if (yo || gx < 0 || gx >= nx) {
+              if (ec.bc == ABFT_BC_CONSTANT) {
+                W[d][t][c2] = ec.g;
+              } else {
+                const int wy = ((gy % ec.ny) + ec.ny) % ec.ny, wx = ((gx % nx) + nx) % nx;
+                W[d][t][c2] = ec.up[d][(size_t)wy * ec.px + wx];
+              }
+            }
+          }
         }
       }
     }
@@ -283,6 +316,11 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   const int nT = (NZ ? ze + 1 : ze) - q0;
   const bool hasP = p.field_src >= 0;
   const bool xedge = (x0 == 0) || (x0 + TX >= nx);            // clamp / ragged columns
+  const bool yedge = (y0 == 0) || (y0 + TY >= ny);
+  const int bc = p.bc;
+  // tiles that build ghosts in registers: clamp -> x-edge tiles (y through
+  // srow); constant / periodic -> every edge tile; zero -> none (TMA zero fill)
+  const bool edge = bc == ABFT_BC_CLAMP ? xedge : (bc == ABFT_BC_ZERO ? false : (xedge || yedge));
   const bool full = (x0 + TX <= nx) && (y0 + TY <= ny);       // no masked cells
   const int64_t px = p.px;
   T* const out_base = reinterpret_cast<T*>(p.out);
@@ -300,7 +338,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     const int st = i % NS;
     mbar_arrive_expect_tx(&barT[st], TL::T_BYTES);
     tma_load_3d(sT + st * TSTR, &tm_u, &barT[st], x0 - HV, y0 - 1,
-                zmap(q0 + i, zc, p.has_lo, p.has_hi));
+                zmap(q0 + i, zc, p.has_lo, p.has_hi, p.bc));
   };
   if (tid == 0)
     for (int i = 0; i < NS && i < nT; ++i) issue_T(i);
@@ -311,7 +349,14 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   const int gyb = y0 + ry0;
   int srow[RY + 2];  // staged row (x HX) of input row gyb - 1 + t, clamped in y
 #pragma unroll
-  for (int t = 0; t < RY + 2; ++t) srow[t] = (max(0, min(gyb - 1 + t, ny - 1)) - y0 + 1) * HX;
+  for (int t = 0; t < RY + 2; ++t)
+    srow[t] = ((bc == ABFT_BC_CLAMP ? max(0, min(gyb - 1 + t, ny - 1)) : gyb - 1 + t) - y0 + 1) * HX;
+  EdgeCtx<T> ec;
+  ec.bc = bc;
+  ec.g = (T)p.g;
+  ec.px = px;
+  ec.gyb = gyb;
+  ec.ny = ny;
   T wr[NP];
   if constexpr (!GEN) {
 #pragma unroll
@@ -345,8 +390,15 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     T out[RY][V];
     if constexpr (!GEN) {
       // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
-      if (xedge) stencil_layer<T, Shape<SS>, RY, NZ, true>(out, pl, srow, wr, lane, gx0, nx);
-      else stencil_layer<T, Shape<SS>, RY, NZ, false>(out, pl, srow, wr, lane, gx0, nx);
+      if (edge) {
+        const T* ub = reinterpret_cast<const T*>(p.uin);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          ec.up[d] = ub + (size_t)(NZ ? zmap(z - 1 + d, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
+        stencil_layer<T, Shape<SS>, RY, NZ, true>(out, pl, srow, wr, lane, gx0, nx, ec);
+      } else {
+        stencil_layer<T, Shape<SS>, RY, NZ, false>(out, pl, srow, wr, lane, gx0, nx, ec);
+      }
     } else {
       // generic radius-1 point list: runtime offsets, identical FMA chain
 #pragma unroll
@@ -357,9 +409,19 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
           for (int q = 0; q < p.npoints; ++q) {
             const int di = p.di[q], dj = p.dj[q], dk = p.dk[q];
             const T* pp = dk < 0 ? pl[0] : (dk > 0 ? pl[2] : pl[1]);
-            const int sr = (max(0, min(gyb + r + dj, ny - 1)) - y0 + 1) * HX;
-            const int sc = max(0, min(gx0 + k + di, nx - 1)) - x0 + HV;
-            const T v = pp[sr + sc];
+            const int yy = gyb + r + dj, xx = gx0 + k + di;
+            T v;
+            if (bc == ABFT_BC_CLAMP || (yy >= 0 && yy < ny && xx >= 0 && xx < nx)) {
+              const int sr = (max(0, min(yy, ny - 1)) - y0 + 1) * HX;
+              const int sc = max(0, min(xx, nx - 1)) - x0 + HV;
+              v = pp[sr + sc];
+            } else if (bc == ABFT_BC_PERIODIC) {
+              const T* ub = reinterpret_cast<const T*>(p.uin) +
+                            (size_t)(NZ ? zmap(z + dk, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
+              v = ub[(size_t)(((yy % ny) + ny) % ny) * px + ((xx % nx) + nx) % nx];
+            } else {
+              v = bc == ABFT_BC_CONSTANT ? (T)p.g : T(0);
+            }
             const T w = pw<T>(p, q);
             acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
           }

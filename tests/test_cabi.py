@@ -80,7 +80,11 @@ def test_workspace_size_sane(L):
     (dict(points=[(0, 0, 0, float("inf"))]), abft.ABFT_EINVAL),
     (dict(mode=2, delta=0), abft.ABFT_EINVAL),
     (dict(mode=7), abft.ABFT_EINVAL),
-    (dict(bc=abft.ABFT_BC_PERIODIC), abft.ABFT_EUNSUPPORTED),
+    (dict(bc=abft.ABFT_BC_PERIODIC, nranks=2, rank=0, z_count=2, nccl_unique_id=b"\0" * 128),
+     abft.ABFT_EUNSUPPORTED),                                  # periodic wrap across ranks
+    (dict(bc=abft.ABFT_BC_CONSTANT, bc_value=float("inf")), abft.ABFT_EINVAL),
+    (dict(bc=9), abft.ABFT_EINVAL),
+    (dict(checksum_policy=2), abft.ABFT_EINVAL),
     (dict(z_begin=1, z_count=2), abft.ABFT_EINVAL),
     (dict(nranks=2, rank=1, z_count=2), abft.ABFT_EINVAL),   # rank 1 cannot own layer 0
     (dict(nranks=2, rank=0, z_count=4), abft.ABFT_EINVAL),   # rank 0 of 2 owns every layer
@@ -90,6 +94,13 @@ def test_workspace_size_validates(L, kw, code):
     with pytest.raises(abft.AbftError) as e:
         abft.abft_stencil_workspace_size(c)
     assert e.value.status == code
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+def test_every_boundary_condition_accepted(L, bc):
+    c, keep = _cfg(bc=bc, bc_value=2.5)
+    fb, ab = abft.abft_stencil_workspace_size(c)
+    assert fb > 0 and ab > 0
 
 
 def test_multi_rank_slab_config_accepted(L):

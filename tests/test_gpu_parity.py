@@ -334,3 +334,70 @@ def test_set_faults_rejects_duplicates_and_overfull_sweeps():
         st.set_faults([Fault(1, z, 0, 0, 20) for z in range(65)])
     st.set_faults([Fault(1, z, 0, 0, 20) for z in range(64)] + [Fault(2, 0, 0, 0, 20)])
     st.destroy()
+
+
+# ---- boundary conditions (P:289-292 clamp; P:407-415 periodic, zero, constant) --
+
+BCS = [(1, 0.0), (2, 0.0), (3, 331.5)]
+
+
+@pytest.mark.parametrize("bc,g", BCS)
+@pytest.mark.parametrize("nx,ny,nz", [(203, 77, 9), (128, 64, 5), (5, 3, 4), (1, 1, 2)])
+def test_bc_hotspot_online(bc, g, nx, ny, nz):
+    p = make_problem("cfg2", nx=nx, ny=ny, nz=nz, sweeps=20, nfaults=0, bc=bc, bc_value=g)
+    faults = [Fault(5, nz - 1, ny - 1, nx - 1, 29), Fault(9, 0, 0, 0, 28), Fault(13, nz // 2, ny // 2, nx // 2, 27)]
+    faults = list({(f.sweep, f.z, f.y, f.x): f for f in faults}.values())
+    parity(p, faults=faults)
+
+
+@pytest.mark.parametrize("bc,g", BCS)
+def test_bc_fig2_five_point_2d(bc, g):
+    p = make_problem("cfg1", nx=70, ny=45, sweeps=20, bc=bc, bc_value=0.25 if bc == 3 else g)
+    parity(p, faults=[Fault(10, 0, 0, 69, 29), Fault(14, 0, 22, 0, 28)])
+
+
+@pytest.mark.parametrize("bc,g", BCS)
+def test_bc_offline_and_lazy(bc, g):
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=24, nfaults=6, mode=2, delta=6, bc=bc, bc_value=g)
+    parity(p)
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=24, nfaults=6, mode=1, bc=bc, bc_value=g,
+                     checksums=1)
+    parity(p, faults=fault_schedule(p) + [Fault(7, 0, 0, 0, 30), Fault(9, 11, 79, 95, 29)])
+
+
+@pytest.mark.parametrize("bc,g", BCS)
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_bc_generic_and_box27(bc, g, dtype):
+    rng = random.Random(bc)
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+    rng.shuffle(offs)
+    w = [rng.uniform(0.01, 1.0) for _ in range(11)]
+    pts = [(a, b, c, v / sum(w)) for (a, b, c), v in zip(offs[:11], w)]
+    p = Problem("gen", 70, 33, 5, dtype, pts, [(0.002, True, 0.0)],
+                eps=1e-5 if dtype == "f32" else 1e-10, mode=1, sweeps=10, init=(1.0, 2.0),
+                power=(0.0, 1.0), bc=bc, bc_value=1.5 if bc == 3 else g)
+    parity(p, faults=[Fault(3, 0, 0, 69, 30 if dtype == "f32" else 62), Fault(7, 4, 32, 0, 29)])
+    q = make_problem("cfg5", nx=40, ny=24, nz=6, sweeps=10, nfaults=4, mode=1, bc=bc, bc_value=0.5 if bc == 3 else g)
+    if dtype == "f64":
+        parity(q)
+
+
+@pytest.mark.parametrize("bc", [2, 3])
+def test_bc_slab_group(bc):
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=1, bc=bc, bc_value=330.0)
+    faults = fault_schedule(p) + [Fault(9, 5, 3, 4, 30), Fault(9, 6, 70, 90, 29)]
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, 3, faults)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+
+
+def test_bc_periodic_multi_rank_unsupported():
+    from paper_1909_00709_b200 import abft
+    p = make_problem("cfg3", nx=64, ny=64, nz=8, bc=1)
+    dev = torch.device("cuda:0")
+    with pytest.raises(abft.AbftError) as e:
+        abft.from_problem(p, field_u0(p, dev)[:4].contiguous(), field_power(p, dev)[:4].contiguous(),
+                          device=dev, z_begin=0, z_count=4, rank=0, nranks=2)
+    assert e.value.status == abft.ABFT_EUNSUPPORTED
