@@ -82,6 +82,41 @@ void or_flip(void* u, int64_t idx, int32_t dtype, int32_t bit) {
  * Fault injection: the flip is applied after the point is updated and
  * before it is stored; since a Jacobi sweep never reads its own output, the
  * flips are applied to the stored values right after the update loop. */
+/* Eq. 1 for one cell (z, y, x) of u^{(t+1)} from u^{(t)} = uin, the
+ * canonical FMA chain (Q23): acc = w0 v0, acc = fma(w_p, v_p, acc) over the
+ * points in order, then acc = fma(coef_q, src_q, acc) over the sources. */
+static double cell_update(const or_problem* p, const void* uin, int64_t z, int64_t y, int64_t x) {
+  const int64_t c = (z * p->ny + y) * p->nx + x;
+  if (p->dtype == OR_F32) {
+    float acc = 0.0f;
+    for (int32_t k = 0; k < p->npoints; k++) {
+      const or_point* q = &p->points[k];
+      float w = (float)q->w;
+      float v = (float)val(p, uin, z + q->dk, y + q->dj, x + q->di);
+      acc = (k == 0) ? w * v : fmaf(w, v, acc);
+    }
+    for (int32_t k = 0; k < p->nsources; k++) {
+      const or_source* s = &p->sources[k];
+      float cf = (float)s->coef;
+      float sv = s->field ? ((const float*)s->field)[c] : (float)s->scalar;
+      acc = fmaf(cf, sv, acc);
+    }
+    return acc;
+  }
+  double acc = 0.0;
+  for (int32_t k = 0; k < p->npoints; k++) {
+    const or_point* q = &p->points[k];
+    double v = val(p, uin, z + q->dk, y + q->dj, x + q->di);
+    acc = (k == 0) ? q->w * v : fma(q->w, v, acc);
+  }
+  for (int32_t k = 0; k < p->nsources; k++) {
+    const or_source* s = &p->sources[k];
+    double sv = s->field ? ((const double*)s->field)[c] : s->scalar;
+    acc = fma(s->coef, sv, acc);
+  }
+  return acc;
+}
+
 void or_sweep(const or_problem* p, const void* uin, void* uout, int64_t sweep,
               or_fault* faults, int64_t nfaults) {
   const int64_t nx = p->nx, ny = p->ny, nz = p->nz;
@@ -89,38 +124,7 @@ void or_sweep(const or_problem* p, const void* uin, void* uout, int64_t sweep,
 #pragma omp parallel for schedule(static)
   for (int64_t zy = 0; zy < nz * ny; zy++) {
     const int64_t z = zy / ny, y = zy % ny;
-    for (int64_t x = 0; x < nx; x++) {
-      const int64_t c = (z * ny + y) * nx + x;
-      if (dt == OR_F32) {
-        float acc = 0.0f;
-        for (int32_t k = 0; k < p->npoints; k++) {
-          const or_point* q = &p->points[k];
-          float w = (float)q->w;
-          float v = (float)val(p, uin, z + q->dk, y + q->dj, x + q->di);
-          acc = (k == 0) ? w * v : fmaf(w, v, acc);
-        }
-        for (int32_t k = 0; k < p->nsources; k++) {
-          const or_source* s = &p->sources[k];
-          float cf = (float)s->coef;
-          float sv = s->field ? ((const float*)s->field)[c] : (float)s->scalar;
-          acc = fmaf(cf, sv, acc);
-        }
-        ((float*)uout)[c] = acc;
-      } else {
-        double acc = 0.0;
-        for (int32_t k = 0; k < p->npoints; k++) {
-          const or_point* q = &p->points[k];
-          double v = val(p, uin, z + q->dk, y + q->dj, x + q->di);
-          acc = (k == 0) ? q->w * v : fma(q->w, v, acc);
-        }
-        for (int32_t k = 0; k < p->nsources; k++) {
-          const or_source* s = &p->sources[k];
-          double sv = s->field ? ((const double*)s->field)[c] : s->scalar;
-          acc = fma(s->coef, sv, acc);
-        }
-        ((double*)uout)[c] = acc;
-      }
-    }
+    for (int64_t x = 0; x < nx; x++) st(uout, (z * ny + y) * nx + x, dt, cell_update(p, uin, z, y, x));
   }
   for (int64_t f = 0; f < nfaults; f++) {
     or_fault* F = &faults[f];
@@ -300,7 +304,7 @@ static void push(or_record* recs, int64_t cap, int64_t* nrec, const or_record* r
  * flagged row and column, correct with Eq. 8 averaged over
  * both checksums (fig.correction) and repair the
  * checksums.  Returns 1 if detected but not corrected. */
-static int32_t check_layer(const or_problem* p, int64_t s, int64_t z, void* u,
+static int32_t check_layer(const or_problem* p, int64_t s, int64_t z, void* u, const void* uprev,
                            double* A, double* B, const double* PA, const double* PB,
                            or_record* recs, int64_t cap, int64_t* nrec, or_stats* st_) {
   const int64_t nx = p->nx, ny = p->ny;
@@ -323,14 +327,16 @@ static int32_t check_layer(const or_problem* p, int64_t s, int64_t z, void* u,
     const int64_t c = (z * ny + y0) * nx + x0;
     const double uo = ld(u, c, p->dtype);
     double vx, vy, cor;
-    if (p->correction_form == 0) {
+    if (p->correction_form == 0 || p->correction_form == 2) {
       /* Eq. 8 with (a - u) evaluated as the sum of the other cells (Q11, Q12) */
       double sx = 0.0, sy = 0.0;
       for (int64_t y = 0; y < ny; y++) if (y != y0) sx += ld(u, (z * ny + y) * nx + x0, p->dtype);
       for (int64_t x = 0; x < nx; x++) if (x != x0) sy += ld(u, (z * ny + y0) * nx + x, p->dtype);
       vx = PA[z * nx + x0] - sx;
       vy = PB[z * ny + y0] - sy;
-      cor = rnd(p->dtype, (vx + vy) / 2.0);
+      /* form 2: stencil locality -- u^(t) is intact, so
+         the located cell is recomputed from it (Eq. 1), exactly */
+      cor = p->correction_form == 2 ? cell_update(p, uprev, z, y0, x0) : rnd(p->dtype, (vx + vy) / 2.0);
       A[z * nx + x0] = sx + cor;
       B[z * ny + y0] = sy + cor;
     } else {
@@ -403,7 +409,7 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
         }
         or_predict(p, Ap, Bp, cur, cA, cB, PA, PB);      /* step 2 */
         for (int64_t z = 0; z < nz; z++)                 /* step 3 + correction */
-          if (check_layer(p, s, z, nxt, An, Bn, PA, PB, recs, cap, nrec, stats)) worst = 1;
+          if (check_layer(p, s, z, nxt, cur, An, Bn, PA, PB, recs, cap, nrec, stats)) worst = 1;
         double* t;
         t = Ap; Ap = An; An = t;
         t = Bp; Bp = Bn; Bn = t;

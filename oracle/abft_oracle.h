@@ -54,7 +54,9 @@ typedef struct {
   const or_point* points;
   const or_source* sources;
   double eps;
-  int32_t mode, delta, correction_form;
+  int32_t mode, delta;
+  int32_t correction_form; /* online: 0 Eq. 8 re-summed (Q11), 1 literal fig.correction,
+                              2 recompute the located cell from u^(t) */
   int32_t checksums;   /* online: 0 = a and b every sweep (SURVEY Q8 reading);
                           1 = b every sweep, a only for layers whose b flags
                           (the paper's recommendation) */

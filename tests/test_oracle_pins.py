@@ -426,6 +426,39 @@ def test_correction_dyadic_is_bitwise_exact():
             assert r["stats"]["detections"] == 1     # repaired checksums: no later flags
 
 
+@pytest.mark.parametrize("name,kw", [
+    ("cfg1", dict(sweeps=12)),
+    ("cfg2", dict(nx=40, ny=33, nz=5, sweeps=12)),
+    ("cfg2", dict(nx=40, ny=33, nz=5, sweeps=12, bc=1)),
+    ("cfg2", dict(nx=40, ny=33, nz=5, sweeps=12, bc=3, bc_value=330.0)),
+    ("cfg5", dict(nx=20, ny=17, nz=5, sweeps=10, mode=1)),
+])
+def test_correction_by_recompute_restores_the_fault_free_run(name, kw):
+    # correction_form 2 (stencil locality): u^(t) is
+    # intact, so recomputing the located cell with Eq. 1 restores it exactly:
+    # every run whose flips are all located equals the fault-free run bitwise
+    # (field and checksums), whatever bit was flipped -- including the exponent
+    # flips that defeat the checksum estimate of Eq. 8.
+    p = make_problem(name, **kw).replace(correction_form=2)
+    fields = [field_power(p).numpy()] if p.power else []
+    op = O.OProblem(p, fields)
+    u0 = field_u0(p).numpy()
+    ref = O.run(op, u0, p.sweeps)
+    rng = random.Random(8)
+    hi = 31 if p.dtype == "f32" else 63
+    done = 0
+    for t in range(30):
+        f = Fault(rng.randint(1, p.sweeps), rng.randrange(p.nz), rng.randrange(p.ny), rng.randrange(p.nx),
+                  rng.randint(hi - 12, hi))
+        r = O.run(op, u0, p.sweeps, [f])
+        if r["stats"]["corrected"] == 1 and r["stats"]["detections"] == 1:
+            w = np.uint32 if p.dtype == "f32" else np.uint64
+            assert (r["u"].view(w) == ref["u"].view(w)).all()
+            assert np.array_equal(r["A"], ref["A"]) or p.dtype == "f64"
+            done += 1
+    assert done >= 15
+
+
 def test_correction_literal_form_fails_on_exponent_flip():
     # "if the bit-flips occur in the last bits of the exponent, the error
     # causes an overflow in the checksums" -- the literal fig.correction form
