@@ -11,7 +11,8 @@ E1 (fig.overhead / fig.error): HotSpot tiles 64x64x8 / 512x512x8,
    the error-free run.
 E2 (fig.biterror): 64x64x8, 128 iterations, for every bit position
    0..31, R flips at random iteration and cell: l2 error quartiles per mode,
-   detection and correction rates.  The paper's findings to compare with:
+   detection and correction rates, for Eq. 8 re-summed, Eq. 8 literal and the
+   locality recompute (correction_form 2).  The paper's findings:
    bits 0-12 never detected, exponent flips break the literal Eq. 8
    correction, offline rollback erases every detected flip.
 E3 (fig.interval): offline detection period 1..128 on both tiles,
@@ -138,7 +139,7 @@ def exp_e1(R: Runner, reps: int, seed: int = 1, policy: int = 0):
     return out
 
 
-def exp_e2(R: Runner, reps: int, seed: int = 2, policy: int = 0, forms=(0, 1)):
+def exp_e2(R: Runner, reps: int, seed: int = 2, policy: int = 0, forms=(0, 1, 2)):
     tile = "64x64x8"
     out = {"exp": "E2 error vs bit position, 64x64x8, 128 iterations (P:852-915)", "policy": policy,
            "reps_per_bit": reps, "bits": {}}
@@ -151,7 +152,8 @@ def exp_e2(R: Runner, reps: int, seed: int = 2, policy: int = 0, forms=(0, 1)):
             for form in (forms if mode == "online" else (0,)):
                 p = problem(tile, mode, correction_form=form)
                 rs = [R.run(p, [f], policy=policy) for f in flips]
-                key = mode if mode != "online" else ("online" if form == 0 else "online_literal_eq8")
+                key = mode if mode != "online" else {0: "online", 1: "online_literal_eq8",
+                                                     2: "online_recompute"}[form]
                 row[key] = {"l2": _q([l2(ref, r["u"]) for r in rs]),
                             "detected": sum(1 for r in rs if r["stats"]["detections"] > 0),
                             "corrected": sum(1 for r in rs if r["stats"]["corrected"] > 0)}

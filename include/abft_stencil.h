@@ -126,7 +126,9 @@ typedef struct {
   int32_t mode;         /* abft_mode */
   int32_t delta;        /* offline detection period, >= 1 */
   int32_t correction_form; /* 0: Eq. 8 with (a - u) re-summed over the other cells
-                              (default); 1: literal fig.correction listing */
+                              (default); 1: literal fig.correction listing; 2: the
+                              located cell recomputed from u^{s-1} with Eq. 1
+                              (stencil locality: exact repair) */
   int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
   int32_t checksum_policy; /* abft_checksum_policy (ONLINE step() only) */
   const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by

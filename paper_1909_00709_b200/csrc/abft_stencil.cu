@@ -143,7 +143,7 @@ int validate(const abft_config* c) {
   if (!(c->epsilon > 0.0) || !isfinite(c->epsilon)) return ABFT_EINVAL;
   if (c->mode < 0 || c->mode > 2) return ABFT_EINVAL;
   if (c->mode == ABFT_MODE_OFFLINE && c->delta < 1) return ABFT_EINVAL;
-  if (c->correction_form != 0 && c->correction_form != 1) return ABFT_EINVAL;
+  if (c->correction_form < 0 || c->correction_form > 2) return ABFT_EINVAL;
   if (c->checksum_policy != ABFT_CK_BOTH && c->checksum_policy != ABFT_CK_LAZY) return ABFT_EINVAL;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
   if (c->nranks > 1) {
@@ -863,6 +863,12 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   for (int q = 0; q < cfg->npoints; ++q) {
     cp.di[q] = sp.di[q]; cp.dj[q] = sp.dj[q]; cp.dk[q] = sp.dk[q]; cp.w[q] = sp.w[q];
   }
+  cp.nsources = cfg->nsources;
+  cp.field_src = h->field_src;
+  for (int q = 0; q < cfg->nsources; ++q) { cp.coef[q] = sp.coef[q]; cp.scalar[q] = sp.scalar[q]; }
+  cp.src = h->src_field;
+  cp.spx = h->src_px;
+  cp.splane = h->src_px * ny;
   cp.eps = cfg->epsilon;
   cp.form = cfg->correction_form;
   cp.z_begin = cfg->z_begin;

@@ -124,6 +124,40 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
   return acc;
 }
 
+// Eq. 1 for the one cell (z, y, x) of u^s from u^{s-1} (p.uprev), with the
+// ghosts of the boundary condition: the same canonical FMA chain as K1
+// (points in order, then the sources).  correction_form 2.
+template <typename T>
+__device__ T cell_update(const CheckParams& p, int z, int y, int x) {
+  const T* up = reinterpret_cast<const T*>(p.uprev);
+  const int nx = p.nx, ny = p.ny, zc = p.zc, bc = p.bc;
+  const T g = bc == ABFT_BC_CONSTANT ? (T)p.g : T(0);
+  T acc = T(0);
+  for (int q = 0; q < p.npoints; ++q) {
+    const int zz = z + p.dk[q], yy = y + p.dj[q], xx = x + p.di[q];
+    T v;
+    const bool yo = yy < 0 || yy >= ny, xo = xx < 0 || xx >= nx;
+    if (zghost(zz, zc, p.has_lo, p.has_hi, bc) ||
+        ((bc == ABFT_BC_ZERO || bc == ABFT_BC_CONSTANT) && (yo || xo))) {
+      v = g;
+    } else {
+      const int bl = zmap(zz, zc, p.has_lo, p.has_hi, bc);
+      const int yr = !yo ? yy : (bc == ABFT_BC_PERIODIC ? wrap(yy, ny) : max(0, min(yy, ny - 1)));
+      const int xr = !xo ? xx : (bc == ABFT_BC_PERIODIC ? wrap(xx, nx) : max(0, min(xx, nx - 1)));
+      v = up[(size_t)bl * p.plane + (size_t)yr * p.px + xr];
+    }
+    const T w = (T)p.w[q];
+    acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
+  }
+  for (int q = 0; q < p.nsources; ++q) {
+    const T sv = q == p.field_src
+                     ? reinterpret_cast<const T*>(p.src)[(size_t)z * p.splane + (size_t)y * p.spx + x]
+                     : (T)p.scalar[q];
+    acc = fma_rn((T)p.coef[q], sv, acc);
+  }
+  return acc;
+}
+
 // Steps (4)-(5) for layer z once its compare is complete (na / nb flagged
 // entries, x0 / y0 the first flagged index, pa / pb their predictions); run by
 // every thread of one CTA of kCheckThreads threads (block-uniform arguments).
@@ -150,7 +184,7 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
     // ---- locate and correct (Eq. 8, fig.correction)
     T* lay = reinterpret_cast<T*>(p.ucur) + (size_t)bz * p.plane;
     double sx = 0.0, sy = 0.0;
-    if (p.form == 0) {   // (a - u) as the sum of the other cells (Q11)
+    if (p.form != 1) {   // (a - u) as the sum of the other cells (Q11)
       for (int y = tid; y < ny; y += kCheckThreads)
         if (y != y0) sx += (double)lay[(size_t)y * p.px + x0];
       for (int x = tid; x < nx; x += kCheckThreads)
@@ -165,10 +199,12 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
       double* by = &p.Bc[(size_t)bz * ny + y0];
       double vx, vy;
       T cor;
-      if (p.form == 0) {
+      if (p.form != 1) {
         vx = pa - sx;
         vy = pb - sy;
-        cor = (T)((vx + vy) / 2.0);
+        // form 2: stencil locality -- u^{s-1} is intact,
+        // the located cell is recomputed with Eq. 1, exactly
+        cor = p.form == 2 ? cell_update<T>(p, z, y0, x0) : (T)((vx + vy) / 2.0);
         *ax = sx + (double)cor;   // exact repair (Q12)
         *by = sy + (double)cor;
       } else {                    // literal listing

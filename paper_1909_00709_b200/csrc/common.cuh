@@ -150,6 +150,10 @@ struct CheckParams {
   int npoints;
   int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
   double w[kMaxPoints];
+  int nsources, field_src;       // the constant term C of Eq. 1 (correction_form 2)
+  double coef[kMaxSources], scalar[kMaxSources];   // rounded to the dtype
+  const void* src;
+  int64_t spx, splane;
   double eps;
   int flags, form;
   long long sweep, z_begin;

@@ -401,3 +401,25 @@ def test_bc_periodic_multi_rank_unsupported():
         abft.from_problem(p, field_u0(p, dev)[:4].contiguous(), field_power(p, dev)[:4].contiguous(),
                           device=dev, z_begin=0, z_count=4, rank=0, nranks=2)
     assert e.value.status == abft.ABFT_EUNSUPPORTED
+
+
+# ---- correction_form 2: recompute the located cell (stencil locality)
+
+@pytest.mark.parametrize("name,kw", [
+    ("cfg1", dict(sweeps=20)),
+    ("cfg2", dict(nx=203, ny=77, nz=9, sweeps=25, nfaults=4)),
+    ("cfg2", dict(nx=128, ny=64, nz=5, sweeps=20, nfaults=3, bc=1)),
+    ("cfg2", dict(nx=128, ny=64, nz=5, sweeps=20, nfaults=3, bc=3, bc_value=330.0)),
+    ("cfg2", dict(nx=96, ny=80, nz=12, sweeps=30, nfaults=8, checksums=1)),
+    ("cfg5", dict(nx=40, ny=24, nz=6, sweeps=10, nfaults=4, mode=1)),
+])
+def test_recompute_correction(name, kw):
+    p = make_problem(name, **kw).replace(correction_form=2)
+    faults = [f for f in fault_schedule(p) if f.bit >= (27 if p.dtype == "f32" else 59)]
+    faults = faults + [Fault(3, 0, 0, 0, 30 if p.dtype == "f32" else 62)]
+    faults = list({(f.sweep, f.z, f.y, f.x): f for f in faults}.values())
+    g, o = parity(p, faults=faults)
+    ref = gpu_run(p, faults=[])
+    if g["stats"]["corrected"] == len(faults):     # every flip located: exact repair
+        w = np.uint32 if p.dtype == "f32" else np.uint64
+        assert np.array_equal(g["u"].view(w), ref["u"].view(w))
