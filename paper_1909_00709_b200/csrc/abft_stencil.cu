@@ -349,7 +349,8 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
     p.faults[p.nfaults++] = LocalFault{(int)zl, (int)pf.f.y, (int)pf.f.x, pf.f.bit};
     pf.fired = true;
   }
-  const bool inj = p.nfaults > 0;
+  // the general K1 instantiation: scheduled flips, constant / periodic ghosts
+  const bool inj = p.nfaults > 0 || h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC;
   h->executed++;
   cudaEvent_t* pe = prof_begin(h, 1);
   cudaError_t e;

@@ -50,7 +50,7 @@ constexpr int kCheckThreads = 128;   // 10+ CTAs per SM: every layer of a 1024-l
 //   a'_x = c_x + sum_S w (a_{zeta(z+k)}[x+i] + alpha_{x+i, j})
 //   b'_y = c_y + sum_S w (b_{zeta(z+k)}[y+j] + beta_{i, y+j})
 // points in the caller's order, fp64, separately rounded; all loads issued first.
-template <typename T, int S, bool A>
+template <typename T, int S, bool A, bool BCG>
 __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int e) {
   constexpr bool GEN = S == SHAPE_GENERIC;
   constexpr int NPM = GEN ? kMaxPoints : Shape<(GEN ? SHAPE_HOTSPOT7 : S)>::NP;
@@ -66,7 +66,7 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
     int di, dj, dk;
     if constexpr (GEN) { di = p.di[q]; dj = p.dj[q]; dk = p.dk[q]; }
     else { di = Shape<S>::off(q, 0); dj = Shape<S>::off(q, 1); dk = Shape<S>::off(q, 2); }
-    const int bc = p.bc;
+    const int bc = BCG ? p.bc : ABFT_BC_CLAMP;   // BCG: periodic / zero / constant ghosts
     const bool ghostv = bc == ABFT_BC_ZERO || bc == ABFT_BC_CONSTANT;
     const double g = bc == ABFT_BC_CONSTANT ? p.g : 0.0;
     const int zq = zmap(z + dk, zc, p.has_lo, p.has_hi, bc);
@@ -247,7 +247,7 @@ constexpr int kCheckUnroll = ABFT_KU;
 // one vector (a' over x if A, else b' over y) of layer z: predict, store the
 // prediction (offline P / explicit check), compare with the actual checksum,
 // clear the generation of sweep s + 2; flags meet in shared memory.
-template <typename T, int S, bool A>
+template <typename T, int S, bool A, bool BCG>
 __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n, int* s_k, double* s_pred,
                                           int part = 0, int nparts = 1) {
   const int nn = A ? p.nx : p.ny, bz = z + 1;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
     for (int u = 0; u < kCheckUnroll; ++u) {
       const int e = e0 + u * kCheckThreads;
       const bool in = e < n;
-      pr[u] = in ? predict_entry<T, S, A>(p, z, e) : 0.0;
+      pr[u] = in ? predict_entry<T, S, A, BCG>(p, z, e) : 0.0;
       ac[u] = (in && cmp) ? act[(size_t)bz * nn + e] : 0.0;
     }
 #pragma unroll
@@ -279,7 +279,7 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
     }
   }
 }
-template <typename T, int S>
+template <typename T, int S, bool BCG>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
   const int z = blockIdx.x, bz = z + 1;
   const int tid = threadIdx.x, part = blockIdx.y, nparts = gridDim.y;
@@ -297,8 +297,8 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
     // round, so the loads of all kCheckUnroll entries are in flight together.
     // Lazy policy: b' only; a is computed by K3 for the
     // layers whose b flags.  nparts > 1 (few layers): this CTA's share.
-    if (!(p.flags & CK_LAZY)) check_vec<T, S, true>(p, z, &s_na, &s_xk, &s_pa, part, nparts);
-    check_vec<T, S, false>(p, z, &s_nb, &s_yk, &s_pb, part, nparts);
+    if (!(p.flags & CK_LAZY)) check_vec<T, S, true, BCG>(p, z, &s_na, &s_xk, &s_pa, part, nparts);
+    check_vec<T, S, false, BCG>(p, z, &s_nb, &s_yk, &s_pb, part, nparts);
     if (!(p.flags & CK_COMPARE)) return;
     __syncthreads();
     if (nparts > 1) {
@@ -375,7 +375,7 @@ __device__ __forceinline__ double col_sum(const T* col, int64_t px, int ny) {
   return s;
 }
 
-template <typename T, int S>
+template <typename T, int S, bool BCG>
 __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__ CheckParams p) {
   __shared__ int s_na, s_xk, s_last;
   __shared__ double s_pa;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
       q.Ap = p.Aw;
       q.PAo = nullptr;
       q.zA = nullptr;
-      check_vec<T, S, true>(q, z, &s_na, &s_xk, &s_pa);
+      check_vec<T, S, true, BCG>(q, z, &s_na, &s_xk, &s_pa);
       __syncthreads();
       const int na = s_na, nb = L->nb;
       const int x0 = na ? 0x7fffffff - s_xk : -1, y0 = 0x7fffffff - L->yk;

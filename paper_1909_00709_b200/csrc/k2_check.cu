@@ -18,14 +18,14 @@ K1Geometry k1y_geometry(int dtype) {
   return {YTile<double>::TX, YTile<double>::TZ, YTile<double>::SMEM, YTile<double>::THREADS};
 }
 
-template <typename T>
+template <typename T, bool BCG>
 static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
   switch (shape) {
-    case SHAPE_FIG2_5PT: k2_check<T, SHAPE_FIG2_5PT><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_FIG2_5PT: k2_check<T, SHAPE_FIG2_5PT, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
     case SHAPE_HOTSPOT7:
-    case SHAPE_HOTSPOT7_FS: k2_check<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
-    case SHAPE_BOX27: k2_check<T, SHAPE_BOX27><<<g, kCheckThreads, 0, s>>>(p); break;
-    default: k2_check<T, SHAPE_GENERIC><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7_FS: k2_check<T, SHAPE_HOTSPOT7, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_BOX27: k2_check<T, SHAPE_BOX27, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    default: k2_check<T, SHAPE_GENERIC, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
   }
   return cudaGetLastError();
 }
@@ -46,17 +46,21 @@ cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckP
     parts = std::max(1, std::min(want, cap));
   }
   const dim3 g(zc, parts);
-  return dtype == ABFT_F32 ? k2_go<float>(shape, g, s, p) : k2_go<double>(shape, g, s, p);
+  // clamp (the paper's fig.sweep boundary) runs instantiations without the
+  // other boundary conditions' branches
+  if (p.bc == ABFT_BC_CLAMP)
+    return dtype == ABFT_F32 ? k2_go<float, false>(shape, g, s, p) : k2_go<double, false>(shape, g, s, p);
+  return dtype == ABFT_F32 ? k2_go<float, true>(shape, g, s, p) : k2_go<double, true>(shape, g, s, p);
 }
 
-template <typename T>
+template <typename T, bool BCG>
 static cudaError_t k3_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
   switch (shape) {
-    case SHAPE_FIG2_5PT: k3_lazy<T, SHAPE_FIG2_5PT><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_FIG2_5PT: k3_lazy<T, SHAPE_FIG2_5PT, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
     case SHAPE_HOTSPOT7:
-    case SHAPE_HOTSPOT7_FS: k3_lazy<T, SHAPE_HOTSPOT7><<<g, kCheckThreads, 0, s>>>(p); break;
-    case SHAPE_BOX27: k3_lazy<T, SHAPE_BOX27><<<g, kCheckThreads, 0, s>>>(p); break;
-    default: k3_lazy<T, SHAPE_GENERIC><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7_FS: k3_lazy<T, SHAPE_HOTSPOT7, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_BOX27: k3_lazy<T, SHAPE_BOX27, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    default: k3_lazy<T, SHAPE_GENERIC, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
   }
   return cudaGetLastError();
 }
@@ -64,7 +68,9 @@ static cudaError_t k3_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
 cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p) {
   // x-tiles x 4 vector kinds x 4 concurrent flagged layers (more loop)
   const dim3 g((p.nx + kCheckThreads - 1) / kCheckThreads, 4, 4);
-  return dtype == ABFT_F32 ? k3_go<float>(shape, g, s, p) : k3_go<double>(shape, g, s, p);
+  if (p.bc == ABFT_BC_CLAMP)
+    return dtype == ABFT_F32 ? k3_go<float, false>(shape, g, s, p) : k3_go<double, false>(shape, g, s, p);
+  return dtype == ABFT_F32 ? k3_go<float, true>(shape, g, s, p) : k3_go<double, true>(shape, g, s, p);
 }
 
 template <typename T>

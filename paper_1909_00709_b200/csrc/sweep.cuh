@@ -19,7 +19,10 @@
 //    the ring), then one fp64 RED per (tile, row) and (tile, column) into the
 //    L2-resident checksum generation -- no extra HBM traffic;
 //  * fault injection flips the value after the update and before the
-//    store, so the checksums see the corrupted value (template INJ).
+//    store, so the checksums see the corrupted value.  Launches with a
+//    scheduled flip, and constant / periodic ghosts, run the GENERAL
+//    instantiation; the hot path (no flip, clamp or zero ghosts) keeps its
+//    registers for the stencil.
 #pragma once
 
 #include "common.cuh"
@@ -153,15 +156,33 @@ template <typename T> struct EdgeCtx {
   int gyb, ny;
 };
 
-template <typename T, class SH, int RY, bool NZ, bool EDGE>
-__device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
-                                              const int (&srow)[RY + 2], const T (&wr)[SH::NP],
-                                              int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
-  constexpr int V = 16 / (int)sizeof(T), TX = 32 * V, HV = V, NP = SH::NP;
-  T W[3][RY + 2][V + 2];
-  // lanes 0 / 31 need the staged halo element left / right of the tile: every
-  // lane loads one of the two (2 addresses, one wavefront), no divergence
+// Byte offsets of a thread's staged rows (loop invariant): sro[t] = its
+// 16-byte vector of staged row t, seo[t] = the halo element lane 0 / 31 needs
+// (every lane loads one of the two: 2 addresses, one wavefront, no
+// divergence).  Added to the layer's slot base, a uniform register, so each
+// shared load is one LDS [R + UR].
+template <int RY> struct RowOffs {
+  int sro[RY + 2], seo[RY + 2];
+};
+template <typename T, int RY>
+__device__ __forceinline__ RowOffs<RY> row_offsets(const int (&srow)[RY + 2], int lane) {
+  constexpr int V = 16 / (int)sizeof(T), TX = 32 * V, HV = V;
   const int eoff = lane == 0 ? HV - 1 : HV + TX;
+  RowOffs<RY> o;
+#pragma unroll
+  for (int t = 0; t < RY + 2; ++t) {
+    o.sro[t] = (srow[t] + HV + lane * V) * (int)sizeof(T);
+    o.seo[t] = (srow[t] + eoff) * (int)sizeof(T);
+  }
+  return o;
+}
+
+template <typename T, class SH, int RY, bool NZ, bool EDGE, bool BCG = true>
+__device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
+                                              const RowOffs<RY>& ro, const T (&wr)[SH::NP],
+                                              int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
+  constexpr int V = 16 / (int)sizeof(T), NP = SH::NP;
+  T W[3][RY + 2][V + 2];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int dk = d - 1;
@@ -173,13 +194,13 @@ __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], cons
       for (int dj = -1; dj <= 1; ++dj)
         if (sh_uses<SH>(dk, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
       if (!need) continue;
-      const T* row = pl[d] + srow[t];
+      const unsigned char* slot = reinterpret_cast<const unsigned char*>(pl[d]);
       T c[V];
-      ld_vec<T, V>(c, row + HV + lane * V);
+      ld_vec<T, V>(c, reinterpret_cast<const T*>(slot + ro.sro[t]));
 #pragma unroll
       for (int k = 0; k < V; ++k) W[d][t][k + 1] = c[k];
       if (sh_uses_x_halo<SH>(dk)) {
-        const T e = row[eoff];
+        const T e = *reinterpret_cast<const T*>(slot + ro.seo[t]);
         T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
         T right = __shfl_down_sync(0xffffffffu, c[0], 1);
         left = lane == 0 ? e : left;
@@ -195,7 +216,7 @@ __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], cons
           }
         }
       }
-      if constexpr (EDGE) {
+      if constexpr (EDGE && BCG) {
         // constant / periodic ghosts (zero ghosts are the TMA's zero fill of
         // out-of-range boxes): every out-of-domain entry of this row
         if (ec.bc == ABFT_BC_CONSTANT || ec.bc == ABFT_BC_PERIODIC) {
@@ -233,25 +254,24 @@ __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], cons
   }
 }
 
-// the source field C (HotSpot power) of layer z for this thread's RY x V
-// cells: read-only 128-bit loads, issued one layer ahead (register prefetch)
-template <typename T, int RY>
-__device__ __forceinline__ void load_src(T (&pv)[RY][16 / sizeof(T)], const SweepParams& p, int z,
-                                         int gyb, int gx0, bool full) {
+// the source field C (HotSpot power) of one layer for this thread's RY x V
+// cells, q = its first cell: read-only 128-bit loads, issued one layer ahead
+// (register prefetch); FULL tiles load without bounds checks
+template <typename T, int RY, bool FULL>
+__device__ __forceinline__ void load_src(T (&pv)[RY][16 / sizeof(T)], const T* q, int64_t spx,
+                                         int gyb, int gx0, int nx, int ny) {
   constexpr int V = 16 / (int)sizeof(T);
   using VT = typename Vec<T>::type;
-  const T* base = reinterpret_cast<const T*>(p.src) + (size_t)z * p.splane + (size_t)gyb * p.spx + gx0;
 #pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    const T* q = base + (size_t)r * p.spx;
-    if (full || (gyb + r < p.ny && gx0 + V <= p.nx)) {
+  for (int r = 0; r < RY; ++r, q += spx) {
+    if (FULL || (gyb + r < ny && gx0 + V <= nx)) {
       VT v = __ldg(reinterpret_cast<const VT*>(q));
       const T* e = reinterpret_cast<const T*>(&v);
 #pragma unroll
       for (int k = 0; k < V; ++k) pv[r][k] = e[k];
     } else {
 #pragma unroll
-      for (int k = 0; k < V; ++k) pv[r][k] = (gyb + r < p.ny && gx0 + k < p.nx) ? __ldg(q + k) : T(0);
+      for (int k = 0; k < V; ++k) pv[r][k] = (gyb + r < ny && gx0 + k < nx) ? __ldg(q + k) : T(0);
     }
   }
 }
@@ -282,10 +302,11 @@ __device__ __forceinline__ void add_sources(T (&out)[RY][16 / sizeof(T)], const 
 }
 
 // K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: which actual
-// checksums the pass accumulates (K1_CK_*).  INJ: apply this launch's
-// scheduled bit-flips.
+// checksums the pass accumulates (K1_CK_*).  GEN_BC: the general
+// instantiation -- applies this launch's scheduled bit-flips and builds
+// constant / periodic ghosts; without it only clamp and zero ghosts.
 // grid (x-tiles, y-tiles, z-chunks); each CTA marches up its z-chunk.
-template <typename T, int S, int CHK, bool INJ>
+template <typename T, int S, int CHK, bool GEN_BC>
 #ifndef ABFT_K1_MINB
 #define ABFT_K1_MINB 2
 #endif
@@ -320,7 +341,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   const int bc = p.bc;
   // tiles that build ghosts in registers: clamp -> x-edge tiles (y through
   // srow); constant / periodic -> every edge tile; zero -> none (TMA zero fill)
-  const bool edge = bc == ABFT_BC_CLAMP ? xedge : (bc == ABFT_BC_ZERO ? false : (xedge || yedge));
+  const bool edge = bc == ABFT_BC_CLAMP ? xedge : ((bc == ABFT_BC_ZERO || !GEN_BC) ? false : (xedge || yedge));
   const bool full = (x0 + TX <= nx) && (y0 + TY <= ny);       // no masked cells
   const int64_t px = p.px;
   T* const out_base = reinterpret_cast<T*>(p.out);
@@ -367,7 +388,16 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   // source-field registers of two consecutive layers, ping-ponged by the
   // 2-way unrolled layer loop below (no register copies per layer)
   T pa[RY][V], pb[RY][V];
-  if (hasP) load_src<T, RY>(pa, p, zs, gyb, gx0, full);
+  const T* psrc = hasP ? reinterpret_cast<const T*>(p.src) + (size_t)zs * p.splane + (size_t)gyb * p.spx + gx0
+                       : nullptr;
+  auto src_layer = [&](T (&dst)[RY][V], const T* q) {
+    if (full) load_src<T, RY, true>(dst, q, p.spx, gyb, gx0, nx, ny);
+    else load_src<T, RY, false>(dst, q, p.spx, gyb, gx0, nx, ny);
+  };
+  if (hasP) src_layer(pa, psrc);
+  // output row of this thread in layer zs (buffer layer zs + 1), advanced per layer
+  T* orow = out_base + (size_t)(zs + 1) * p.plane + (size_t)gyb * px + gx0;
+  const RowOffs<RY> ro = row_offsets<T, RY>(srow, lane);
 
   auto layer = [&](const int z, T (&pv)[RY][V], T (&pn)[RY][V]) {
     const int it = z - zs;
@@ -385,19 +415,21 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       mbar_wait(&barT[it % NS], (it / NS) & 1);
       pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
     }
-    if (hasP && z + 1 < ze) load_src<T, RY>(pn, p, z + 1, gyb, gx0, full);
+    if (hasP && z + 1 < ze) src_layer(pn, psrc + (size_t)(it + 1) * p.splane);
 
     T out[RY][V];
     if constexpr (!GEN) {
       // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
       if (edge) {
-        const T* ub = reinterpret_cast<const T*>(p.uin);
+        if constexpr (GEN_BC) {
+          const T* ub = reinterpret_cast<const T*>(p.uin);
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-          ec.up[d] = ub + (size_t)(NZ ? zmap(z - 1 + d, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
-        stencil_layer<T, Shape<SS>, RY, NZ, true>(out, pl, srow, wr, lane, gx0, nx, ec);
+          for (int d = 0; d < 3; ++d)
+            ec.up[d] = ub + (size_t)(NZ ? zmap(z - 1 + d, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
+        }
+        stencil_layer<T, Shape<SS>, RY, NZ, true, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
       } else {
-        stencil_layer<T, Shape<SS>, RY, NZ, false>(out, pl, srow, wr, lane, gx0, nx, ec);
+        stencil_layer<T, Shape<SS>, RY, NZ, false, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
       }
     } else {
       // generic radius-1 point list: runtime offsets, identical FMA chain
@@ -411,7 +443,8 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
             const T* pp = dk < 0 ? pl[0] : (dk > 0 ? pl[2] : pl[1]);
             const int yy = gyb + r + dj, xx = gx0 + k + di;
             T v;
-            if (bc == ABFT_BC_CLAMP || (yy >= 0 && yy < ny && xx >= 0 && xx < nx)) {
+            if (bc == ABFT_BC_CLAMP || (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ||
+                (!GEN_BC && bc != ABFT_BC_ZERO)) {
               const int sr = (max(0, min(yy, ny - 1)) - y0 + 1) * HX;
               const int sc = max(0, min(xx, nx - 1)) - x0 + HV;
               v = pp[sr + sc];
@@ -430,7 +463,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       }
     }
     add_sources<T, RY, FS>(out, pv, p, c0, c1, s1);   // constant term C of Eq. 1
-    if constexpr (INJ) {  // after the update, before the store
+    if constexpr (GEN_BC) {  // after the update, before the store
       for (int f = 0; f < p.nfaults; ++f) {
         const LocalFault F = p.faults[f];
         if (F.z != z) continue;
@@ -442,7 +475,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       }
     }
     // store (128-bit where the vector is whole)
-    T* obase = out_base + (size_t)(z + 1) * p.plane + (size_t)gyb * px + gx0;
+    T* obase = orow + (size_t)it * p.plane;
     using VT = typename Vec<T>::type;
     if (full) {
 #pragma unroll

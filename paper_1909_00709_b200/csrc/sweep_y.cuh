@@ -177,8 +177,9 @@ __global__ void __launch_bounds__(YTile<T>::THREADS, 1)
       if constexpr (!GEN) {
         EdgeCtx<T> ec{};          // the y-march runs clamp only
         ec.bc = ABFT_BC_CLAMP;
-        if (xedge) stencil_layer<T, SH, RZ, true, true>(out, pl, srow, wr, lane, gx0, nx, ec);
-        else stencil_layer<T, SH, RZ, true, false>(out, pl, srow, wr, lane, gx0, nx, ec);
+        const RowOffs<RZ> ro = row_offsets<T, RZ>(srow, lane);
+        if (xedge) stencil_layer<T, SH, RZ, true, true>(out, pl, ro, wr, lane, gx0, nx, ec);
+        else stencil_layer<T, SH, RZ, true, false>(out, pl, ro, wr, lane, gx0, nx, ec);
       } else {
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
