@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   int na, nb, xk, yk;
   double pa, pb;
   (void)bz;
+  grid_dependency_wait();   // K1's checksums and field (PDL)
   if (!(p.flags & CK_FROM_SUMMARY)) {
     if (tid == 0) { s_na = 0; s_nb = 0; s_xk = 0; s_yk = 0; s_pa = 0.0; s_pb = 0.0; }
     __syncthreads();
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
   __shared__ double s_pa;
   __shared__ double red[kCheckThreads / 32];
   const int tid = threadIdx.x, nx = p.nx, ny = p.ny, zc = p.zc;
+  grid_dependency_wait();   // K2's layer list (PDL)
   const int n = *(volatile int*)&p.st->lazy_n[p.sweep & 1];
   // the next sweep's K2 counts into the other slot: clear it (nobody reads it now)
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)

@@ -20,14 +20,15 @@ K1Geometry k1y_geometry(int dtype) {
 
 template <typename T, bool BCG>
 static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
+  cudaError_t e = cudaSuccess;
   switch (shape) {
-    case SHAPE_FIG2_5PT: k2_check<T, SHAPE_FIG2_5PT, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_FIG2_5PT: e = launch_pdl(k2_check<T, SHAPE_FIG2_5PT, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
     case SHAPE_HOTSPOT7:
-    case SHAPE_HOTSPOT7_FS: k2_check<T, SHAPE_HOTSPOT7, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
-    case SHAPE_BOX27: k2_check<T, SHAPE_BOX27, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
-    default: k2_check<T, SHAPE_GENERIC, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7_FS: e = launch_pdl(k2_check<T, SHAPE_HOTSPOT7, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
+    case SHAPE_BOX27: e = launch_pdl(k2_check<T, SHAPE_BOX27, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
+    default: e = launch_pdl(k2_check<T, SHAPE_GENERIC, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p) {
@@ -55,14 +56,15 @@ cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckP
 
 template <typename T, bool BCG>
 static cudaError_t k3_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {
+  cudaError_t e = cudaSuccess;
   switch (shape) {
-    case SHAPE_FIG2_5PT: k3_lazy<T, SHAPE_FIG2_5PT, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_FIG2_5PT: e = launch_pdl(k3_lazy<T, SHAPE_FIG2_5PT, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
     case SHAPE_HOTSPOT7:
-    case SHAPE_HOTSPOT7_FS: k3_lazy<T, SHAPE_HOTSPOT7, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
-    case SHAPE_BOX27: k3_lazy<T, SHAPE_BOX27, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
-    default: k3_lazy<T, SHAPE_GENERIC, BCG><<<g, kCheckThreads, 0, s>>>(p); break;
+    case SHAPE_HOTSPOT7_FS: e = launch_pdl(k3_lazy<T, SHAPE_HOTSPOT7, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
+    case SHAPE_BOX27: e = launch_pdl(k3_lazy<T, SHAPE_BOX27, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
+    default: e = launch_pdl(k3_lazy<T, SHAPE_GENERIC, BCG>, g, dim3(kCheckThreads), 0, s, p); break;
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p) {

@@ -2,9 +2,30 @@
 // per dtype for K1 so the template instantiations compile in parallel).
 #pragma once
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace abft {
+
+// launch with programmatic stream serialization (PDL): the grid may be
+// scheduled while the previous kernel on the stream drains; the kernel calls
+// grid_dependency_wait() before it reads that kernel's results
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 struct K1Geometry {
   int tile_x, tile_y, smem, threads;

@@ -310,6 +310,9 @@ template <typename T, int S, int CHK, bool GEN_BC>
 #ifndef ABFT_K1_MINB
 #define ABFT_K1_MINB 2
 #endif
+#ifndef ABFT_ROWS_DEFERRED
+#define ABFT_ROWS_DEFERRED 1
+#endif
 __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABFT_K1_MINB)
     k1_sweep(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ SweepParams p) {
   using TL = Tile<T>;
@@ -354,6 +357,9 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     for (int i = 0; i < NS; ++i) mbar_init(&barT[i], 1);
     fence_mbar_init();
   }
+  // the previous sweep's check kernels may still correct u^{s-1} or read the
+  // buffer this sweep writes: wait for them (PDL) after the setup above
+  grid_dependency_wait();
   __syncthreads();
   auto issue_T = [&](int i) {
     const int st = i % NS;
@@ -399,6 +405,14 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   T* orow = out_base + (size_t)(zs + 1) * p.plane + (size_t)gyb * px + gx0;
   const RowOffs<RY> ro = row_offsets<T, RY>(srow, lane);
 
+  double rsp[RY];   // row partials of the previous layer, pending reduction
+  int zprev = -1;
+  auto flush_rows = [&](int zl) {
+    const double tot = row_reduce<RY>(rsp, lane);
+    const int gy = gyb + row_of_lane<RY>(lane);
+    if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(zl + 1) * ny + gy], tot);
+  };
+  (void)flush_rows;
   auto layer = [&](const int z, T (&pv)[RY][V], T (&pn)[RY][V]) {
     const int it = z - zs;
     const T* pl[3];
@@ -462,6 +476,11 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
         }
       }
     }
+#if ABFT_ROWS_DEFERRED
+    if constexpr (CHK != K1_CK_NONE) {
+      if (zprev >= 0) flush_rows(zprev);   // b of the previous layer (Eq. 3)
+    }
+#endif
     add_sources<T, RY, FS>(out, pv, p, c0, c1, s1);   // constant term C of Eq. 1
     if constexpr (GEN_BC) {  // after the update, before the store
       for (int f = 0; f < p.nfaults; ++f) {
@@ -529,10 +548,18 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
         if (full) row_sums<T, true>(out, rs, gyb, gx0, nx, ny);
         else row_sums<T, false>(out, rs, gyb, gx0, nx, ny);
       }
+#if ABFT_ROWS_DEFERRED
+      // the warp reduction of these row partials runs in the next layer's body
+      // (off this layer's critical path; its shuffles overlap the next stencil)
+#pragma unroll
+      for (int r = 0; r < RY; ++r) rsp[r] = rs[r];
+      zprev = z;
+#else
       // b^s_y += sum over this tile's columns (Eq. 3)
       const double tot = row_reduce<RY>(rs, lane);
       const int gy = gyb + row_of_lane<RY>(lane);
       if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(z + 1) * ny + gy], tot);
+#endif
       if constexpr (CHK == K1_CK_AB) {
         // column partials of this layer; double-buffered, so the one barrier per
         // layer below also orders them against the reduction two layers later
@@ -563,6 +590,11 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     layer(z + 1, pb, pa);
   }
   if (z < ze) layer(z, pa, pb);
+#if ABFT_ROWS_DEFERRED
+  if constexpr (CHK != K1_CK_NONE) {
+    if (zprev >= 0) flush_rows(zprev);
+  }
+#endif
 }
 
 }  // namespace abft
