@@ -349,8 +349,11 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
     p.faults[p.nfaults++] = LocalFault{(int)zl, (int)pf.f.y, (int)pf.f.x, pf.f.bit};
     pf.fired = true;
   }
-  // the general K1 instantiation: scheduled flips, constant / periodic ghosts
-  const bool inj = p.nfaults > 0 || h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC;
+  // K1 variant: constant / periodic ghosts need the general one; scheduled
+  // flips the injecting one; everything else runs the hot path
+  const bool inj = p.nfaults > 0;
+  const int var = (h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC) ? K1_GEN
+                  : (inj ? K1_INJ : K1_HOT);
   h->executed++;
   cudaEvent_t* pe = prof_begin(h, 1);
   cudaError_t e;
@@ -360,8 +363,8 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
             : launch_k1y_f64(h->shape, chk == K1_CK_AB, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p);
   else
     e = h->cfg.dtype == ABFT_F32
-            ? launch_k1_f32(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], p)
-            : launch_k1_f64(h->shape, chk, inj, h->grid1, h->stream, h->tm_u[src], p);
+            ? launch_k1_f32(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p)
+            : launch_k1_f64(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p);
   prof_end(h, pe);
   h->launches++;
   CK(e);

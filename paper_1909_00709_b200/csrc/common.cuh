@@ -80,6 +80,9 @@ template <int S> struct SwapYZ {
   }
 };
 
+// K1 instantiation variants: hot path, with scheduled bit-flips, general
+enum K1Variant { K1_HOT = 0, K1_INJ = 1, K1_GEN = 2 };
+
 // which actual checksums K1 accumulates in its pass
 enum K1Checksums { K1_CK_NONE = 0, K1_CK_AB = 1 /* a and b */, K1_CK_B = 2 /* b only (lazy a) */ };
 

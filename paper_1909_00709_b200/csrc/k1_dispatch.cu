@@ -3,25 +3,25 @@
 
 namespace abft {
 
-cudaError_t launch_k1_f32(int shape, int chk, bool inj, dim3 grid, cudaStream_t s, const CUtensorMap& tu,
+cudaError_t launch_k1_f32(int shape, int chk, int var, dim3 grid, cudaStream_t s, const CUtensorMap& tu,
                           const SweepParams& p) {
   switch (shape) {
-    case SHAPE_FIG2_5PT: return launch_k1_f32_s1(chk, inj, grid, s, tu, p);
-    case SHAPE_HOTSPOT7: return launch_k1_f32_s2(chk, inj, grid, s, tu, p);
-    case SHAPE_BOX27: return launch_k1_f32_s3(chk, inj, grid, s, tu, p);
-    case SHAPE_HOTSPOT7_FS: return launch_k1_f32_s4(chk, inj, grid, s, tu, p);
-    default: return launch_k1_f32_s0(chk, inj, grid, s, tu, p);
+    case SHAPE_FIG2_5PT: return launch_k1_f32_s1(chk, var, grid, s, tu, p);
+    case SHAPE_HOTSPOT7: return launch_k1_f32_s2(chk, var, grid, s, tu, p);
+    case SHAPE_BOX27: return launch_k1_f32_s3(chk, var, grid, s, tu, p);
+    case SHAPE_HOTSPOT7_FS: return launch_k1_f32_s4(chk, var, grid, s, tu, p);
+    default: return launch_k1_f32_s0(chk, var, grid, s, tu, p);
   }
 }
 
-cudaError_t launch_k1_f64(int shape, int chk, bool inj, dim3 grid, cudaStream_t s, const CUtensorMap& tu,
+cudaError_t launch_k1_f64(int shape, int chk, int var, dim3 grid, cudaStream_t s, const CUtensorMap& tu,
                           const SweepParams& p) {
   switch (shape) {
-    case SHAPE_FIG2_5PT: return launch_k1_f64_s1(chk, inj, grid, s, tu, p);
-    case SHAPE_HOTSPOT7: return launch_k1_f64_s2(chk, inj, grid, s, tu, p);
-    case SHAPE_BOX27: return launch_k1_f64_s3(chk, inj, grid, s, tu, p);
-    case SHAPE_HOTSPOT7_FS: return launch_k1_f64_s4(chk, inj, grid, s, tu, p);
-    default: return launch_k1_f64_s0(chk, inj, grid, s, tu, p);
+    case SHAPE_FIG2_5PT: return launch_k1_f64_s1(chk, var, grid, s, tu, p);
+    case SHAPE_HOTSPOT7: return launch_k1_f64_s2(chk, var, grid, s, tu, p);
+    case SHAPE_BOX27: return launch_k1_f64_s3(chk, var, grid, s, tu, p);
+    case SHAPE_HOTSPOT7_FS: return launch_k1_f64_s4(chk, var, grid, s, tu, p);
+    default: return launch_k1_f64_s0(chk, var, grid, s, tu, p);
   }
 }
 

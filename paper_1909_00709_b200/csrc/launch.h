@@ -34,13 +34,13 @@ K1Geometry k1_geometry(int dtype);
 // y-march (3D shapes): tile_x x tile_y = x-columns x z-layers of one tile
 K1Geometry k1y_geometry(int dtype);
 
-cudaError_t launch_k1_f32(int shape, int chk, bool inj, dim3 grid, cudaStream_t s,
+cudaError_t launch_k1_f32(int shape, int chk, int var, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
-cudaError_t launch_k1_f64(int shape, int chk, bool inj, dim3 grid, cudaStream_t s,
+cudaError_t launch_k1_f64(int shape, int chk, int var, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
 // per (dtype, shape) translation units (k1_<dtype>_s<shape>.cu)
 #define ABFT_K1_DECL(name) \
-  cudaError_t name(int chk, bool inj, dim3 grid, cudaStream_t s, const CUtensorMap& tu, const SweepParams& p);
+  cudaError_t name(int chk, int var, dim3 grid, cudaStream_t s, const CUtensorMap& tu, const SweepParams& p);
 ABFT_K1_DECL(launch_k1_f32_s0) ABFT_K1_DECL(launch_k1_f32_s1) ABFT_K1_DECL(launch_k1_f32_s2)
 ABFT_K1_DECL(launch_k1_f32_s3) ABFT_K1_DECL(launch_k1_f32_s4)
 ABFT_K1_DECL(launch_k1_f64_s0) ABFT_K1_DECL(launch_k1_f64_s1) ABFT_K1_DECL(launch_k1_f64_s2)

@@ -302,11 +302,11 @@ __device__ __forceinline__ void add_sources(T (&out)[RY][16 / sizeof(T)], const 
 }
 
 // K1.  S: ShapeId (SHAPE_GENERIC = runtime point list).  CHK: which actual
-// checksums the pass accumulates (K1_CK_*).  GEN_BC: the general
-// instantiation -- applies this launch's scheduled bit-flips and builds
-// constant / periodic ghosts; without it only clamp and zero ghosts.
+// checksums the pass accumulates (K1_CK_*).  VAR: K1_HOT (clamp / zero
+// ghosts, no flips), K1_INJ (+ this launch's scheduled bit-flips), K1_GEN
+// (+ constant / periodic ghosts).
 // grid (x-tiles, y-tiles, z-chunks); each CTA marches up its z-chunk.
-template <typename T, int S, int CHK, bool GEN_BC>
+template <typename T, int S, int CHK, int VAR>
 #ifndef ABFT_K1_MINB
 #define ABFT_K1_MINB 2
 #endif
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   const int bc = p.bc;
   // tiles that build ghosts in registers: clamp -> x-edge tiles (y through
   // srow); constant / periodic -> every edge tile; zero -> none (TMA zero fill)
+  constexpr bool GEN_BC = VAR == K1_GEN, INJ = VAR != K1_HOT;
   const bool edge = bc == ABFT_BC_CLAMP ? xedge : ((bc == ABFT_BC_ZERO || !GEN_BC) ? false : (xedge || yedge));
   const bool full = (x0 + TX <= nx) && (y0 + TY <= ny);       // no masked cells
   const int64_t px = p.px;
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     }
 #endif
     add_sources<T, RY, FS>(out, pv, p, c0, c1, s1);   // constant term C of Eq. 1
-    if constexpr (GEN_BC) {  // after the update, before the store
+    if constexpr (INJ) {  // after the update, before the store
       for (int f = 0; f < p.nfaults; ++f) {
         const LocalFault F = p.faults[f];
         if (F.z != z) continue;
