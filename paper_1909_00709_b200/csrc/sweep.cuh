@@ -42,11 +42,14 @@ template <typename T> struct Tile {
 #ifndef ABFT_RY_F32
 #define ABFT_RY_F32 4
 #endif
+#ifndef ABFT_RY_F64
+#define ABFT_RY_F64 4
+#endif
 #ifndef ABFT_NS
 #define ABFT_NS 4
 #endif
 
-  static constexpr int RY = sizeof(T) == 4 ? ABFT_RY_F32 : 2;  // output rows per thread
+  static constexpr int RY = sizeof(T) == 4 ? ABFT_RY_F32 : ABFT_RY_F64;  // output rows per thread
   static constexpr int TY = WARPS * RY;
   static constexpr int ROWS = TY + 2;
   static constexpr int T_BYTES = ROWS * HX * (int)sizeof(T);
@@ -177,8 +180,33 @@ __device__ __forceinline__ RowOffs<RY> row_offsets(const int (&srow)[RY + 2], in
   return o;
 }
 
+// Plane groups of a point list: maximal runs of consecutive points on the
+// same staged plane (HotSpot: {c,w,e,n,s}, {t}, {b}; 27-point box: 3 x 9).
+template <class SH> __host__ __device__ constexpr int group_end(int q) {
+  int e = q;
+  while (e < SH::NP && SH::off(e, 2) == SH::off(q, 2)) ++e;
+  return e;
+}
+template <class SH> __host__ __device__ constexpr bool group_uses_row(int q, int dj) {
+  for (int e = q; e < group_end<SH>(q); ++e)
+    if (SH::off(e, 1) == dj) return true;
+  return false;
+}
+template <class SH> __host__ __device__ constexpr bool group_uses_halo(int q) {
+  for (int e = q; e < group_end<SH>(q); ++e)
+    if (SH::off(e, 0) != 0) return true;
+  return false;
+}
+
+// One layer of one thread: RY x V outputs of Eq. 1, the canonical FMA chain
+// in the point order.  The points are applied plane group by plane group: a
+// group's staged rows are loaded (with the x halo and the ghosts of an edge
+// tile) into one register plane, then every output's chain advances through
+// the group's points -- only one plane is live, so the 27-point box fits.
+// All three planes loaded first, then the chains (few points per plane:
+// every load in flight at once; the HotSpot 7-point path).
 template <typename T, class SH, int RY, bool NZ, bool EDGE, bool BCG = true>
-__device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
+__device__ __forceinline__ void stencil_layer_all(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
                                               const RowOffs<RY>& ro, const T (&wr)[SH::NP],
                                               int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
   constexpr int V = 16 / (int)sizeof(T), NP = SH::NP;
@@ -252,6 +280,89 @@ __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], cons
       out[r][k] = acc;
     }
   }
+}
+
+// Plane by plane (many points per plane: the 27-point box).
+template <typename T, class SH, int RY, bool NZ, bool EDGE, bool BCG = true>
+__device__ __forceinline__ void stencil_layer_grouped(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
+                                                      const RowOffs<RY>& ro, const T (&wr)[SH::NP],
+                                                      int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
+  constexpr int V = 16 / (int)sizeof(T), NP = SH::NP;
+  T W[RY + 2][V + 2];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int dk = SH::off(q, 2), d = dk + 1;
+    if (q == 0 || SH::off(q - 1, 2) != dk) {
+      // ---- load the rows of plane dk this group reads
+#pragma unroll
+      for (int t = 0; t < RY + 2; ++t) {
+        bool need = false;
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj)
+          if (group_uses_row<SH>(q, dj) && t - 1 - dj >= 0 && t - 1 - dj < RY) need = true;
+        if (!need) continue;
+        const unsigned char* slot = reinterpret_cast<const unsigned char*>(pl[NZ ? d : 1]);
+        T c[V];
+        ld_vec<T, V>(c, reinterpret_cast<const T*>(slot + ro.sro[t]));
+#pragma unroll
+        for (int k = 0; k < V; ++k) W[t][k + 1] = c[k];
+        if (group_uses_halo<SH>(q)) {
+          const T e = *reinterpret_cast<const T*>(slot + ro.seo[t]);
+          T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+          T right = __shfl_down_sync(0xffffffffu, c[0], 1);
+          left = lane == 0 ? e : left;
+          right = lane == 31 ? e : right;
+          W[t][0] = left;
+          W[t][V + 1] = right;
+          if constexpr (EDGE) {
+            if (ec.bc == ABFT_BC_CLAMP) {
+              if (gx0 == 0) W[t][0] = W[t][1];
+#pragma unroll
+              for (int c2 = 1; c2 < V + 2; ++c2)
+                if (gx0 - 1 + c2 >= nx) W[t][c2] = W[t][c2 - 1];
+            }
+          }
+        }
+        if constexpr (EDGE && BCG) {
+          // constant / periodic ghosts (zero ghosts are the TMA's zero fill of
+          // out-of-range boxes): every out-of-domain entry of this row
+          if (ec.bc == ABFT_BC_CONSTANT || ec.bc == ABFT_BC_PERIODIC) {
+            const int gy = ec.gyb - 1 + t;
+            const bool yo = gy < 0 || gy >= ec.ny;
+#pragma unroll
+            for (int c2 = 0; c2 < V + 2; ++c2) {
+              const int gx = gx0 - 1 + c2;
+              if (yo || gx < 0 || gx >= nx) {
+                if (ec.bc == ABFT_BC_CONSTANT) {
+                  W[t][c2] = ec.g;
+                } else {
+                  const int wy = ((gy % ec.ny) + ec.ny) % ec.ny, wx = ((gx % nx) + nx) % nx;
+                  W[t][c2] = ec.up[NZ ? d : 1][(size_t)wy * ec.px + wx];
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    // ---- every output's chain advances by point q
+    const int di = SH::off(q, 0), dj = SH::off(q, 1);
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const T v = W[r + 1 + dj][k + 1 + di];
+        out[r][k] = (q == 0) ? mul_rn(wr[q], v) : fma_rn(wr[q], v, out[r][k]);
+      }
+  }
+}
+
+template <typename T, class SH, int RY, bool NZ, bool EDGE, bool BCG = true>
+__device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
+                                              const RowOffs<RY>& ro, const T (&wr)[SH::NP],
+                                              int lane, int gx0, int nx, const EdgeCtx<T>& ec) {
+  if constexpr (SH::NP > 9) stencil_layer_grouped<T, SH, RY, NZ, EDGE, BCG>(out, pl, ro, wr, lane, gx0, nx, ec);
+  else stencil_layer_all<T, SH, RY, NZ, EDGE, BCG>(out, pl, ro, wr, lane, gx0, nx, ec);
 }
 
 // the source field C (HotSpot power) of one layer for this thread's RY x V

@@ -11,6 +11,10 @@ if name != "base":
 cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg4"
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 p = make_problem(cfg)
+if len(sys.argv) > 4:
+    p = p.replace(nz=int(sys.argv[4]))
+if p.mode == 2:
+    p = p.replace(mode=1)   # per-sweep K1/K2 times: online
 dev = torch.device("cuda:0")
 u0, P = field_u0(p, dev), field_power(p, dev)
 res = {"lib": name}
