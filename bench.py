@@ -180,13 +180,20 @@ def run_ours(a):
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    nccl_id = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+
+    def handle_kw():
+        # every handle gets its own communicator, so a fresh ncclUniqueId from
+        # rank 0 (an id is good for one ncclCommInitRank rendezvous)
+        nccl_id = None
+        if world > 1:
+            import torch.distributed as dist
+            obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+        return dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
     p = make_problem(a.config)
     if not a.strong:            # weak scaling: each rank owns a slab of the config's size
         per = a.nz_per_gpu or (128 if a.config == "cfg5" else p.nz)
@@ -202,14 +209,13 @@ def run_ours(a):
     u0 = field_u0(p, dev, z0, zc)
     P = field_power(p, dev, z0, zc)
     faults = fault_schedule(p, K)
-    kw = dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
     vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
     idx = vis.split(",")[local] if vis and vis.split(",")[local].isdigit() else str(local)
     clocks = Clocks(idx)
 
     def protected_run(mode, with_faults, prof=False, policy=pol):
         st = abft.from_problem(p, u0, P, device=dev, stream=stream, mode=mode,
-                               checksum_policy=policy, **kw)
+                               checksum_policy=policy, **handle_kw())
         if with_faults:
             st.set_faults(shift(faults, W))
         st.step(W)
@@ -288,7 +294,8 @@ def run_ours(a):
         def job():
             if Pd is not None:
                 Pd.copy_(Ph, non_blocking=True)
-            st = abft.from_problem(p, u0h, Pd, device=dev, stream=stream, checksum_policy=pol, **kw)
+            st = abft.from_problem(p, u0h, Pd, device=dev, stream=stream, checksum_policy=pol,
+                                   **handle_kw())
             st.set_faults(faults)
             st.step(K)
             st.read_field(outh)
