@@ -177,7 +177,7 @@ Layout layout(const abft_config* c) {
   L.off_cB = take((size_t)c->z_count * c->ny * 8);
   for (int b = 0; b < 3; ++b) L.off_EX[b] = take((size_t)2 * zc2 * c->ny * L.esz);
   L.off_summ = take((size_t)c->z_count * sizeof(LayerSummary));
-  L.off_lazy = take((size_t)c->z_count * sizeof(int));
+  L.off_lazy = take((size_t)c->z_count * sizeof(int) + (size_t)4 * zc2 * sizeof(int));
   L.off_st = take(sizeof(DevState));
   L.hot_bytes = o;
   for (int g = 0; g < 2; ++g) { L.off_PA[g] = take(zc2 * c->nx * 8); L.off_PB[g] = take(zc2 * c->ny * 8); }
@@ -215,6 +215,8 @@ struct abft_stencil {
   double *cA, *cB;
   LayerSummary* summ;
   int* lazy_list;
+  int* lazy_rowlist;
+  int* lazy_mark;
   DevState* st;
   const void* src_field = nullptr;
   int64_t src_px = 0;
@@ -734,6 +736,8 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->cB = reinterpret_cast<double*>(h->aux + L.off_cB);
   h->summ = reinterpret_cast<LayerSummary*>(h->aux + L.off_summ);
   h->lazy_list = reinterpret_cast<int*>(h->aux + L.off_lazy);
+  h->lazy_rowlist = h->lazy_list + cfg->z_count;
+  h->lazy_mark = h->lazy_rowlist + 2 * (cfg->z_count + 2);
   for (int b = 0; b < 3; ++b) h->EX[b] = h->aux + L.off_EX[b];
   h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
   h->has_lo = cfg->rank > 0;
@@ -863,6 +867,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   cp.bc = cfg->bc;
   cp.g = sp.g;
   cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st; cp.lazy_list = h->lazy_list;
+  cp.lazy_rowlist = h->lazy_rowlist; cp.lazy_mark = h->lazy_mark;
   cp.npoints = cfg->npoints;
   for (int q = 0; q < cfg->npoints; ++q) {
     cp.di[q] = sp.di[q]; cp.dj[q] = sp.dj[q]; cp.dk[q] = sp.dk[q]; cp.w[q] = sp.w[q];
@@ -888,6 +893,22 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
         return fail(ABFT_ECUDA);
     }
   }
+
+  // load every kernel variant this handle may launch (hot / flip / general K1
+  // for each checksum mode, K2, K3) now: with CUDA's lazy module loading the
+  // first sweep carrying a flip would otherwise pay the load inside the run
+  if (!h->ymarch) {
+    const int vars[3] = {K1_HOT, K1_INJ, K1_GEN};
+    const int chks[3] = {K1_CK_NONE, K1_CK_AB, K1_CK_B};
+    for (int ci = 0; ci < 3; ++ci)
+      for (int vi = 0; vi < 3; ++vi) {
+        const cudaError_t e = cfg->dtype == ABFT_F32
+                                  ? launch_k1_f32(h->shape, chks[ci], vars[vi], dim3(0), h->stream, h->tm_u[0], sp)
+                                  : launch_k1_f64(h->shape, chks[ci], vars[vi], dim3(0), h->stream, h->tm_u[0], sp);
+        if (e != cudaSuccess) return fail(ABFT_ECUDA);
+      }
+  }
+  if (prime_checks(cfg->dtype, h->shape, cfg->bc) != cudaSuccess) return fail(ABFT_ECUDA);
 
   // K0: trusted a^0, b^0 of u0 and the pre-computed c_x, c_y
   if (launch_k0_field(cfg->dtype, h->fb[0], L.px, L.plane, (int)nx, (int)ny, (int)zc, h->gA[0], h->gB[0],

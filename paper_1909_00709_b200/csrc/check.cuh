@@ -327,9 +327,27 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
       na = s_na; nb = s_nb; xk = s_xk; yk = s_yk; pa = s_pa; pb = s_pb;
     }
     if (p.flags & CK_LAZY) {      // hand the flagged layer to K3
-      if (nb && tid == 0) {
-        L->nb = nb; L->yk = yk; L->pb = pb; L->cnt = 0;
-        p.lazy_list[atomicAdd(&p.st->lazy_n[p.sweep & 1], 1)] = z;
+      if (nb) {
+        // the rows of a this layer's check reads: a^{s-1} of zeta(z-1), z,
+        // zeta(z+1) and a^s of z -- each marked once (a neighbour layer may
+        // need the same row), zeroed for K3's partial sums, listed
+        __shared__ int s_new[4], s_row[4];
+        if (tid == 0) {
+          L->nb = nb; L->yk = yk; L->pb = pb;
+          p.lazy_list[atomicAdd(&p.st->lazy_n[p.sweep & 1], 1)] = z;
+          for (int k = 0; k < 4; ++k) {
+            const int sel = k == 3, bl = sel ? z + 1 : zmap(z + k - 1, p.zc, p.has_lo, p.has_hi, p.bc);
+            s_row[k] = (sel << 30) | bl;
+            s_new[k] = atomicCAS(&p.lazy_mark[sel * (p.zc + 2) + bl], 0, 1) == 0;
+            if (s_new[k]) p.lazy_rowlist[atomicAdd(&p.st->lazy_rows[p.sweep & 1], 1)] = s_row[k];
+          }
+        }
+        __syncthreads();
+        for (int k = 0; k < 4; ++k) {
+          if (!s_new[k]) continue;
+          double* row = ((s_row[k] >> 30) ? p.Ac : p.Aw) + (size_t)(s_row[k] & 0x3fffffff) * p.nx;
+          for (int x = tid; x < p.nx; x += kCheckThreads) row[x] = 0.0;
+        }
       }
       return;
     }
@@ -351,77 +369,89 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
 }
 
-// K3 (lazy checksum policy): for every layer z whose b flagged in K2, the
+// K3 (lazy checksum policy): for the layers whose b flagged in K2, the
 // second checksum vector "only in case of error, to enable correction"
 // (P:271-273): a^{s-1} of the layers the prediction reads
-// (zeta(z-1), z, zeta(z+1), column sums of u^{s-1}, halo layers included) and
-// a^s of z (column sums of u^s), each column summed sequentially in
-// ascending y like Eq. 2; then the CTA that completes the layer predicts a'
-// (Theorem 1), compares, locates and corrects as K2 does for policy BOTH.
-// grid (ceil(nx / kCheckThreads), 4 vector kinds, slot stride); exits at once
-// when no layer flagged.  Layer lists alternate by sweep parity: K3 of sweep s
-// clears the count of sweep s + 1 before K2 of s + 1 appends to it.
-template <typename T>
-__device__ __forceinline__ double col_sum(const T* col, int64_t px, int ny) {
-  double s = 0.0;
-  int y = 0;
-  for (; y + 8 <= ny; y += 8) {
-    T v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = col[(size_t)(y + j) * px];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s += (double)v[j];
-  }
-  for (; y < ny; ++y) s += (double)col[(size_t)y * px];
-  return s;
-}
-
+// (zeta(z-1), z, zeta(z+1): column sums of u^{s-1}, halo layers included) and
+// a^s of z (of u^s).  K2 marked each needed row once, zeroed it and listed it;
+// here every CTA (x-tile, row chunk) adds its chunk's column partials into the
+// listed rows (fp64 RED: exact for fp32 data, like the z-march), and the CTA
+// that finishes last predicts a' (Theorem 1), compares, locates and corrects
+// each flagged layer as K2 does for policy BOTH, then clears the marks.
+// Exits at once when no layer flagged.  Lists alternate by sweep parity: K3 of
+// sweep s clears the counts of sweep s + 1 before K2 of s + 1 appends.
 template <typename T, int S, bool BCG>
 __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__ CheckParams p) {
   __shared__ int s_na, s_xk, s_last;
   __shared__ double s_pa;
   __shared__ double red[kCheckThreads / 32];
   const int tid = threadIdx.x, nx = p.nx, ny = p.ny, zc = p.zc;
-  grid_dependency_wait();   // K2's layer list (PDL)
-  const int n = *(volatile int*)&p.st->lazy_n[p.sweep & 1];
+  grid_dependency_wait();   // K2's lists (PDL)
+  const int par = p.sweep & 1;
+  const int n = *(volatile int*)&p.st->lazy_n[par];
+  const int nrows = *(volatile int*)&p.st->lazy_rows[par];
   // the next sweep's K2 counts into the other slot: clear it (nobody reads it now)
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
-    p.st->lazy_n[(p.sweep + 1) & 1] = 0;
-  const int kind = blockIdx.y;   // 0, 1, 2: a^{s-1} of zeta(z-1), z, zeta(z+1); 3: a^s of z
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    p.st->lazy_n[par ^ 1] = 0;
+    p.st->lazy_rows[par ^ 1] = 0;
+  }
+  if (n == 0) return;
+  // ---- column partials of this CTA's x-tile and row chunk, every listed row
   const int x = blockIdx.x * kCheckThreads + tid;
-  for (int i = blockIdx.z; i < n; i += gridDim.z) {
+  const int chunk = (ny + gridDim.y - 1) / gridDim.y;
+  const int y0c = blockIdx.y * chunk, y1c = min(ny, y0c + chunk);
+  if (x < nx) {
+    for (int i = 0; i < nrows; ++i) {
+      const int e = p.lazy_rowlist[i];
+      const int sel = e >> 30, bl = e & 0x3fffffff;   // sel 0: a^{s-1} (u^{s-1}), 1: a^s (u^s)
+      const T* col = reinterpret_cast<const T*>(sel ? p.ucur : p.uprev) + (size_t)bl * p.plane + x;
+      double part = 0.0;
+      int y = y0c;
+      for (; y + 8 <= y1c; y += 8) {
+        T v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = col[(size_t)(y + j) * p.px];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) part += (double)v[j];
+      }
+      for (; y < y1c; ++y) part += (double)col[(size_t)y * p.px];
+      if (y1c > y0c) atomicAdd((sel ? p.Ac : p.Aw) + (size_t)bl * nx + x, part);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(&p.st->lazy_done, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- the last CTA: steps (2)-(5) for a of every flagged layer
+  for (int i = 0; i < n; ++i) {
     const int z = p.lazy_list[i];
     LayerSummary* L = &p.summ[z];
-    const int bl = kind == 3 ? z + 1 : zmap(z + kind - 1, zc, p.has_lo, p.has_hi, p.bc);
-    const T* u = reinterpret_cast<const T*>(kind == 3 ? p.ucur : p.uprev);
-    double* dst = (kind == 3 ? p.Ac : p.Aw) + (size_t)bl * nx;
-    if (x < nx) dst[x] = col_sum<T>(u + (size_t)bl * p.plane + x, p.px, ny);
+    if (tid == 0) { s_na = 0; s_xk = 0; s_pa = 0.0; }
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(&L->cnt, 1) == 4 * (int)gridDim.x - 1;
-    }
+    CheckParams q = p;
+    q.flags = CK_COMPARE;
+    q.Ap = p.Aw;
+    q.PAo = nullptr;
+    q.zA = nullptr;
+    check_vec<T, S, true, BCG>(q, z, &s_na, &s_xk, &s_pa);
     __syncthreads();
-    if (s_last) {
-      __threadfence();
-      if (tid == 0) { s_na = 0; s_xk = 0; s_pa = 0.0; }
-      __syncthreads();
-      CheckParams q = p;
-      q.flags = CK_COMPARE;
-      q.Ap = p.Aw;
-      q.PAo = nullptr;
-      q.zA = nullptr;
-      check_vec<T, S, true, BCG>(q, z, &s_na, &s_xk, &s_pa);
-      __syncthreads();
-      const int na = s_na, nb = L->nb;
-      const int x0 = na ? 0x7fffffff - s_xk : -1, y0 = 0x7fffffff - L->yk;
-      const double pa = s_pa, pb = L->pb;
-      __syncthreads();
-      if (tid == 0) { L->nb = 0; L->yk = 0; L->cnt = 0; }
-      finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
-    }
+    const int na = s_na, nb = L->nb;
+    const int x0 = na ? 0x7fffffff - s_xk : -1, y0 = 0x7fffffff - L->yk;
+    const double pa = s_pa, pb = L->pb;
+    __syncthreads();
+    if (tid == 0) { L->nb = 0; L->yk = 0; }
+    finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
     __syncthreads();
   }
+  for (int i = tid; i < nrows; i += kCheckThreads) {   // marks of this sweep's rows
+    const int e = p.lazy_rowlist[i];
+    p.lazy_mark[(e >> 30) * (zc + 2) + (e & 0x3fffffff)] = 0;
+  }
+  if (tid == 0) p.st->lazy_done = 0;
 }
 
 // ---------------------------------------------------------------- K0

@@ -100,6 +100,8 @@ struct DevState {
   long long flag_a, flag_b;  // explicit check(): flagged entries
   long long ncorr;           // explicit correct(): corrections
   int lazy_n[2];             // lazy checksum policy: layers whose b flagged, by sweep parity
+  int lazy_rows[2];          // lazy policy: a rows to compute, by sweep parity
+  int lazy_done;             // lazy policy: K3 CTAs finished
   abft_record rec[kRecordCap];
 };
 enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCORR,
@@ -110,7 +112,7 @@ enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCO
 struct LayerSummary {
   int na, nb;      // flagged entries of a (over x) and b (over y)
   int xk, yk;      // max of (INT_MAX - index) over flagged entries: the first flagged index
-  int cnt;         // lazy policy: K3 CTAs done with this layer's a vectors
+  int cnt;         // spare
   int cnt2;        // K2 CTAs of this layer done (split layers, gridDim.y > 1)
   double pa, pb;   // predicted a'_{x0}, b'_{y0} (meaningful when na == 1 / nb == 1)
 };
@@ -150,6 +152,8 @@ struct CheckParams {
   DevState* st;
   double* Aw;          // lazy policy: a^{s-1} written by K3 (the predictor input generation)
   int* lazy_list;      // lazy policy: flagged layers of this sweep, [zc]
+  int* lazy_rowlist;   // lazy policy: (sel << 30 | buffer layer) of the a rows K3 sums, [2 (zc+2)]
+  int* lazy_mark;      // lazy policy: row already listed this sweep, [2][zc+2]
   int npoints;
   int di[kMaxPoints], dj[kMaxPoints], dk[kMaxPoints];
   double w[kMaxPoints];

@@ -68,8 +68,10 @@ static cudaError_t k3_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
 }
 
 cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p) {
-  // x-tiles x 4 vector kinds x 4 concurrent flagged layers (more loop)
-  const dim3 g((p.nx + kCheckThreads - 1) / kCheckThreads, 4, 4);
+  // x-tiles x row chunks of >= 32 rows (at most 16): the column sums of a
+  // flagged layer's a rows spread over ~ntx x 16 CTAs
+  const int chunks = std::max(1, std::min(16, (p.ny + 31) / 32));
+  const dim3 g((p.nx + kCheckThreads - 1) / kCheckThreads, chunks);
   if (p.bc == ABFT_BC_CLAMP)
     return dtype == ABFT_F32 ? k3_go<float, false>(shape, g, s, p) : k3_go<double, false>(shape, g, s, p);
   return dtype == ABFT_F32 ? k3_go<float, true>(shape, g, s, p) : k3_go<double, true>(shape, g, s, p);
@@ -85,6 +87,31 @@ cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t 
   const int blocks = (int)std::min<int64_t>(1184, (n + 255) / 256);
   if (dtype == ABFT_F32) fill_value<float><<<blocks, 256, 0, s>>>(static_cast<float*>(ptr), n, (float)v);
   else fill_value<double><<<blocks, 256, 0, s>>>(static_cast<double*>(ptr), n, v);
+  return cudaGetLastError();
+}
+
+// load every check kernel a handle of (dtype, shape, bc) may launch, so the
+// first flagged sweep does not pay CUDA's lazy module loading
+template <typename T, int S, bool BCG>
+static void prime_one() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k2_check<T, S, BCG>);
+  cudaFuncGetAttributes(&a, k3_lazy<T, S, BCG>);
+}
+template <typename T, bool BCG>
+static void prime_shape(int shape) {
+  switch (shape) {
+    case SHAPE_FIG2_5PT: prime_one<T, SHAPE_FIG2_5PT, BCG>(); break;
+    case SHAPE_HOTSPOT7:
+    case SHAPE_HOTSPOT7_FS: prime_one<T, SHAPE_HOTSPOT7, BCG>(); break;
+    case SHAPE_BOX27: prime_one<T, SHAPE_BOX27, BCG>(); break;
+    default: prime_one<T, SHAPE_GENERIC, BCG>(); break;
+  }
+}
+cudaError_t prime_checks(int dtype, int shape, int bc) {
+  const bool g = bc != ABFT_BC_CLAMP;
+  if (dtype == ABFT_F32) g ? prime_shape<float, true>(shape) : prime_shape<float, false>(shape);
+  else g ? prime_shape<double, true>(shape) : prime_shape<double, false>(shape);
   return cudaGetLastError();
 }
 

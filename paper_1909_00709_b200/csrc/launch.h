@@ -56,6 +56,8 @@ int k1y_occ_f64(int shape);
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
 // fill n elements of a field buffer with v (constant ghost layers)
 cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t s);
+// load the check kernels of (dtype, shape, bc) now (CUDA lazy module loading)
+cudaError_t prime_checks(int dtype, int shape, int bc);
 // K3 (lazy checksum policy)
 cudaError_t launch_k3(int dtype, int shape, cudaStream_t s, const CheckParams& p);
 // K0: A[z + off][x] / B[z + off][y] sums of the field buffer `u`
