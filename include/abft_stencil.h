@@ -202,9 +202,14 @@ int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
 /* Local group: n handles created by THIS process for the n slabs of one
  * domain (cfg.nranks = n, cfg.rank = i, cfg.nccl_unique_id = NULL, slabs
  * contiguous in rank order), on one GPU or on several peer GPUs.  group()
- * links them and exchanges the initial halo; their halos then move by device
- * copies (cudaMemcpyAsync, peer copies over NVLink across GPUs) ordered with
- * events across the handles' streams, instead of NCCL.  step_group() runs n
+ * links them and exchanges the initial halo.  Halos then move inside the
+ * kernels (fused halo): K1 stores each slab's boundary layers
+ * also into the neighbours' halo layers, K2/K3 store the boundary layers'
+ * checksum (or offline prediction) rows and any correction there too --
+ * straight to the neighbour's memory (same device, or a peer GPU over NVLink
+ * with peer access enabled by group()); events order each slab's next sweep
+ * after its neighbours' sweep.  ABFT_GROUP_COPY=1, GPUs without peer access,
+ * or the y-march fall back to device copies after each sweep.  step_group() runs n
  * protected sweeps of every slab in lockstep (offline: windows, verdicts and
  * rollbacks are collective).  abft_stencil_step / _sweep / _check / _correct
  * reject grouped handles (ABFT_EINVAL).  Destroying a member dissolves the

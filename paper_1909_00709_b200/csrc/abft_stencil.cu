@@ -255,6 +255,12 @@ struct abft_stencil {
   abft_stencil* hi_peer = nullptr;
   bool grouped = false;
   std::vector<abft_stencil*> members;
+  // fused halo (local group): the sweep's kernels store the boundary layers,
+  // their checksum / prediction rows and corrections straight into the
+  // neighbours' halo slots; fwd_* name what crosses a face this sweep
+  bool fused = false;
+  int fwd_buf = -1, fwd_kind = 0, fwd_idx = 0;
+  int dev = 0;
   cudaEvent_t ev_ready = nullptr, ev_pulled = nullptr;
   // measurement hook: event pairs around K1 / K2 launches
   bool prof = false;
@@ -316,6 +322,8 @@ int match_shape(const abft_config* c) {
 double rnd(int dtype, double v) { return dtype == ABFT_F32 ? (double)(float)v : v; }
 
 // steps (2)-(5) parameters for one sweep (see CheckParams)
+constexpr int XV_GEN_ID = 1, XV_P_ID = 2;   // = XV_GEN, XV_P below
+
 CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, const double* Bp,
                        double* Ac, double* Bc, double* PAo, double* PBo, double* zA, double* zB,
                        int flags, int64_t sweep) {
@@ -327,6 +335,23 @@ CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, c
   p.EXc = h->EX[ucur];
   p.flags = flags;
   p.sweep = sweep;
+  for (int f = 0; f < 2; ++f) { p.peerU[f] = nullptr; p.fwdA[f] = p.fwdB[f] = nullptr; }
+  if (h->fused && h->fwd_buf == ucur) {
+    abft_stencil* nb[2] = {h->lo_peer, h->hi_peer};
+    const size_t lb = (size_t)h->L.plane * h->L.esz;
+    for (int f = 0; f < 2; ++f) {
+      abft_stencil* q = nb[f];
+      if (!q) continue;
+      const int64_t row = f == 0 ? q->cfg.z_count + 1 : 0;   // the neighbour's halo slot
+      p.peerU[f] = q->fb[ucur] + (size_t)row * lb;
+      double *qa = nullptr, *qb = nullptr;
+      if (h->fwd_kind == XV_GEN_ID) { qa = q->gA[h->fwd_idx]; qb = q->gB[h->fwd_idx]; }
+      if (h->fwd_kind == XV_P_ID) { qa = q->PA[h->fwd_idx]; qb = q->PB[h->fwd_idx]; }
+      // lazy policy: a rows are K3 scratch, recomputed from the field by the neighbour
+      if (qa && !(flags & CK_LAZY)) p.fwdA[f] = qa + (size_t)row * q->cfg.nx;
+      if (qb) p.fwdB[f] = qb + (size_t)row * q->cfg.ny;
+    }
+  }
   return p;
 }
 
@@ -335,6 +360,12 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
   SweepParams p = h->sp;
   p.out = h->fb[dst];
   p.uin = h->fb[src];
+  p.peerU[0] = p.peerU[1] = nullptr;
+  if (h->fused && h->fwd_buf == dst) {
+    const size_t lb = (size_t)h->L.plane * h->L.esz;
+    if (h->lo_peer) p.peerU[0] = h->lo_peer->fb[dst] + (size_t)(h->lo_peer->cfg.z_count + 1) * lb;
+    if (h->hi_peer) p.peerU[1] = h->hi_peer->fb[dst];
+  }
   p.EX = h->cfg.mode != ABFT_MODE_NONE ? h->EX[dst] : nullptr;
   p.A = A;
   p.B = B;
@@ -487,16 +518,43 @@ int exchange_local(Group& G, const XSpec& x) {
   return ABFT_OK;
 }
 
+// fused halo: the kernels already wrote every neighbour's halo; order the next
+// sweep of each slab after this sweep of its neighbours
+int sync_local(Group& G) {
+  for (abft_stencil* h : G) CK(cudaEventRecord(h->ev_ready, h->stream));
+  for (abft_stencil* h : G)
+    for (abft_stencil* q : {h->lo_peer, h->hi_peer})
+      if (q) CK(cudaStreamWaitEvent(h->stream, q->ev_ready, 0));
+  return ABFT_OK;
+}
+
+// what crosses the faces of this sweep, for the fused halo (set before launching)
+void set_fwd(Group& G, const XSpec& x) {
+  for (abft_stencil* h : G) {
+    h->fwd_buf = h->fused ? x.buf : -1;
+    h->fwd_kind = x.kind;
+    h->fwd_idx = x.idx;
+  }
+}
+
 int halo_exchange(Group& G, const XSpec& x) {
+  if (G.size() > 1 && G[0]->fused) {
+    for (abft_stencil* h : G) h->fwd_buf = -1;
+    return sync_local(G);
+  }
   if (G.size() > 1) return exchange_local(G, x);
   abft_stencil* h = G[0];
   if (h->cfg.nranks == 1) return ABFT_OK;
   return exchange_nccl(h, x);
 }
 
+// the interior rows of a checksum generation, which K1 accumulates into; the
+// halo rows belong to the neighbours' exchange (a fused neighbour may already
+// have written them on its own stream)
 int zero_gen(abft_stencil* h, int g) {
-  CK(cudaMemsetAsync(h->gA[g], 0, sizeof(double) * (h->cfg.z_count + 2) * h->cfg.nx, h->stream));
-  CK(cudaMemsetAsync(h->gB[g], 0, sizeof(double) * (h->cfg.z_count + 2) * h->cfg.ny, h->stream));
+  const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
+  CK(cudaMemsetAsync(h->gA[g] + nx, 0, sizeof(double) * zc * nx, h->stream));
+  CK(cudaMemsetAsync(h->gB[g] + ny, 0, sizeof(double) * zc * ny, h->stream));
   return ABFT_OK;
 }
 
@@ -514,6 +572,7 @@ int online_sweep(Group& G) {
   const int64_t s = h0->sweeps + 1;
   const int src = h0->cur, dst = 1 - h0->cur;
   const int gp = h0->gen, gn = (h0->gen + 1) % 3, gz = (h0->gen + 2) % 3;
+  set_fwd(G, XSpec{dst, XV_GEN, gn});
   for (abft_stencil* h : G) {
     if (!h->next_zero) TRY(zero_gen(h, gn));
     if (h->cfg.checksum_policy == ABFT_CK_LAZY) {
@@ -548,6 +607,7 @@ int none_sweep(Group& G) {
   abft_stencil* h0 = G[0];
   const int64_t s = h0->sweeps + 1;
   const int src = h0->cur, dst = 1 - h0->cur;
+  set_fwd(G, XSpec{dst, XV_NONE, 0});
   for (abft_stencil* h : G) TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
   TRY(halo_exchange(G, XSpec{dst, XV_NONE, 0}));
   for (abft_stencil* h : G) {
@@ -599,6 +659,7 @@ int offline_window(Group& G, int L) {
       const int64_t s = s0 + t;
       const int dst = (src == others[0]) ? others[1] : others[0];
       const bool end = (t == L);
+      set_fwd(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1});
       // P^{t-1}: the checkpoint's actual checksums for t = 1, else slot (t-1)&1
       for (abft_stencil* h : G) {
         const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
@@ -747,6 +808,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   auto fail = [&](int code) { delete h; return code; };
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(ABFT_ECUDA);
+  h->dev = dev;
   if (!encode_fn()) return fail(ABFT_ECUDA);
 
   // field: u0 (host or device, dense) -> buffer 0 layers 1..zc (padded pitch)
@@ -947,11 +1009,34 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
     if (h->sweeps != 0) return ABFT_EINVAL;
   }
   Group G(hs, hs + n);
+  // fused halo when every neighbour's memory is directly addressable: same
+  // device, or a peer GPU with peer access (NVLink); ABFT_GROUP_COPY=1 keeps
+  // the device-copy exchange
+  bool fused = !(getenv("ABFT_GROUP_COPY") && getenv("ABFT_GROUP_COPY")[0] == '1');
+  for (int i = 0; i < n; ++i) fused = fused && !hs[i]->ymarch;   // the y-march K1 stores locally only
+  int cur_dev = 0;
+  CK(cudaGetDevice(&cur_dev));
+  for (int i = 0; i + 1 < n && fused; ++i) {
+    const int a = hs[i]->dev, b = hs[i + 1]->dev;
+    if (a == b) continue;
+    int ab = 0, ba = 0;
+    cudaDeviceCanAccessPeer(&ab, a, b);
+    cudaDeviceCanAccessPeer(&ba, b, a);
+    if (!ab || !ba) { fused = false; break; }
+    for (int pr = 0; pr < 2; ++pr) {
+      CK(cudaSetDevice(pr ? b : a));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(pr ? a : b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) fused = false;
+      cudaGetLastError();
+    }
+  }
+  CK(cudaSetDevice(cur_dev));
   for (int i = 0; i < n; ++i) {
     abft_stencil* h = hs[i];
     h->lo_peer = i > 0 ? hs[i - 1] : nullptr;
     h->hi_peer = i + 1 < n ? hs[i + 1] : nullptr;
     h->grouped = true;
+    h->fused = fused;
     h->members = G;
     CK(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_pulled, cudaEventDisableTiming));

@@ -215,6 +215,12 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
         *by += (double)cor - uo;
       }
       *cell = cor;
+      for (int f = 0; f < 2; ++f) {   // fused halo: the neighbours' copies
+        if (z != (f == 0 ? 0 : zc - 1)) continue;
+        if (p.peerU[f]) reinterpret_cast<T*>(p.peerU[f])[(size_t)y0 * p.px + x0] = cor;
+        if (p.fwdA[f]) p.fwdA[f][x0] = *ax;
+        if (p.fwdB[f]) p.fwdB[f][y0] = *by;
+      }
       if (p.EXc) {   // keep the edge ledger of u^s in step with the field
         T* exc = reinterpret_cast<T*>(p.EXc);
         if (x0 == 0) exc[(size_t)bz * ny + y0] = cor;
@@ -256,6 +262,11 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
   double* pout = A ? p.PAo : p.PBo;
   double* zero = A ? p.zA : p.zB;
   const bool cmp = p.flags & CK_COMPARE;
+  // fused halo: this layer's rows the neighbours need (predictions when they
+  // are stored, else the actual checksums)
+  double* fwd0 = z == 0 ? (A ? p.fwdA[0] : p.fwdB[0]) : nullptr;
+  double* fwd1 = z == p.zc - 1 ? (A ? p.fwdA[1] : p.fwdB[1]) : nullptr;
+  const bool fwd_pred = p.flags & CK_STORE_PRED;
   for (int e0 = lo + threadIdx.x; e0 < n; e0 += kCheckThreads * kCheckUnroll) {
     double pr[kCheckUnroll], ac[kCheckUnroll];
 #pragma unroll
@@ -276,6 +287,11 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
         *s_pred = pr[u];
       }
       if (zero) zero[(size_t)bz * nn + e] = 0.0;
+      if (fwd0 || fwd1) {
+        const double v = fwd_pred ? pr[u] : act[(size_t)bz * nn + e];
+        if (fwd0) fwd0[e] = v;
+        if (fwd1) fwd1[e] = v;
+      }
     }
   }
 }

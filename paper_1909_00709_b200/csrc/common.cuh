@@ -151,6 +151,9 @@ struct CheckParams {
   LayerSummary* summ;  // [zc]
   DevState* st;
   double* Aw;          // lazy policy: a^{s-1} written by K3 (the predictor input generation)
+  void* peerU[2];      // fused halo: neighbours' halo layer of ucur (corrections), or null
+  double* fwdA[2];     // fused halo: neighbours' halo row of the checksums / predictions
+  double* fwdB[2];     //   this kernel produces for layer 0 ([0]) and zc-1 ([1]), or null
   int* lazy_list;      // lazy policy: flagged layers of this sweep, [zc]
   int* lazy_rowlist;   // lazy policy: (sel << 30 | buffer layer) of the a rows K3 sums, [2 (zc+2)]
   int* lazy_mark;      // lazy policy: row already listed this sweep, [2][zc+2]
@@ -175,6 +178,8 @@ struct SweepParams {
   int bc;              // abft_bc of Eq. 1's ghosts
   double g;            // ghost value (ABFT_BC_CONSTANT), rounded to the dtype
   const void* uin;     // input field buffer (periodic wrap reads at tile edges)
+  void* peerU[2];      // fused halo: the lower / upper neighbour's halo layer in its
+                       // copy of `out` (local group, same or peer GPU), or null
   void* out;           // output field buffer (layer 0 = lower halo)
   double* A;           // checksum generation accumulated by this sweep, [(zc+2)][nx]
   double* B;           // [(zc+2)][ny]

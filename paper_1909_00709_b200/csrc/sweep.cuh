@@ -635,6 +635,29 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
         }
       }
     }
+    // fused halo (local group): the boundary layers also go straight into the
+    // neighbours' halo layer (same device, or a peer GPU over NVLink)
+    for (int f = 0; f < 2; ++f) {
+      T* ph = reinterpret_cast<T*>(p.peerU[f]);
+      if (!ph || z != (f == 0 ? 0 : zc - 1)) continue;
+      T* pbase = ph + (size_t)gyb * px + gx0;
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        if (gyb + r >= ny) continue;
+        T* o = pbase + (size_t)r * px;
+        if (full || gx0 + V <= nx) {
+          VT v;
+          T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+          for (int k = 0; k < V; ++k) e[k] = out[r][k];
+          *reinterpret_cast<VT*>(o) = v;
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (gx0 + k < nx) o[k] = out[r][k];
+        }
+      }
+    }
     // ledger for Theorem 1's beta terms of the next check: the x-edge columns
     if (exl && xedge) {
       const size_t lay = (size_t)(z + 1) * ny;

@@ -221,9 +221,21 @@ def _group_run(p, G, faults, uneven=False):
     return dict(u=u, records=recs, stats=stats, status=status, A=A, B=B)
 
 
+@pytest.fixture(params=["fused", "copy"])
+def halo(request, monkeypatch):
+    """Local groups exchange halos either inside the kernels (fused: boundary
+    layers, checksum rows and corrections stored into the neighbours' slots)
+    or by device copies after each sweep (ABFT_GROUP_COPY=1)."""
+    if request.param == "copy":
+        monkeypatch.setenv("ABFT_GROUP_COPY", "1")
+    else:
+        monkeypatch.delenv("ABFT_GROUP_COPY", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("G,uneven", [(2, False), (2, True), (3, False), (4, False)])
 @pytest.mark.parametrize("mode", [1, 2])
-def test_slab_group_equals_oracle(G, uneven, mode, march):
+def test_slab_group_equals_oracle(G, uneven, mode, march, halo):
     # SURVEY §8(e): per-layer arithmetic does not depend on the partition, so
     # any z-slab decomposition is bitwise identical to the single domain.
     from tests.parity_util import assert_records_equal
@@ -242,7 +254,7 @@ def test_slab_group_equals_oracle(G, uneven, mode, march):
         assert sum(s[k] for s in g["stats"]) == o["stats"][k]
 
 
-def test_slab_group_fp64_box27_offline(march):
+def test_slab_group_fp64_box27_offline(march, halo):
     from tests.parity_util import assert_records_equal
     p = make_problem("cfg5", nx=70, ny=33, nz=9, sweeps=15, nfaults=6)
     faults = fault_schedule(p)
@@ -312,7 +324,7 @@ def test_lazy_cfg5_reduced_fp64_box27_online():
 
 
 @pytest.mark.parametrize("G", [2, 3])
-def test_lazy_slab_group_equals_oracle(G):
+def test_lazy_slab_group_equals_oracle(G, halo):
     from tests.parity_util import assert_records_equal
     p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=1, checksums=1)
     faults = fault_schedule(p) + [Fault(9, 5, 3, 4, 30), Fault(9, 6, 70, 90, 29), Fault(11, 4, 0, 0, 30)]
@@ -383,7 +395,7 @@ def test_bc_generic_and_box27(bc, g, dtype):
 
 
 @pytest.mark.parametrize("bc", [2, 3])
-def test_bc_slab_group(bc):
+def test_bc_slab_group(bc, halo):
     from tests.parity_util import assert_records_equal
     p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=1, bc=bc, bc_value=330.0)
     faults = fault_schedule(p) + [Fault(9, 5, 3, 4, 30), Fault(9, 6, 70, 90, 29)]
