@@ -254,12 +254,15 @@ int64_t abft_stencil_sweep_count(const abft_stencil* h);
 /* Kernel launches issued by this handle so far (for launch accounting). */
 int64_t abft_stencil_launch_count(const abft_stencil* h);
 
-/* Measurement hook.  enable != 0: every K1 (fused sweep + checksums) and K2
- * (predict / compare / locate / correct) launch is bracketed by CUDA events
- * on the handle's stream.  profile_read synchronises, returns the summed
- * device time (ms) and launch counts of each kernel since the last read, and
- * resets them.  Also reports the K1 launch geometry (grid x, y, z, threads
- * per CTA, dynamic shared memory bytes, layers per CTA) when geo != NULL. */
+/* Measurement hook.  enable != 0: every K1 (fused sweep + checksums) launch
+ * and every check launch -- K2 (predict / compare / locate / correct) and,
+ * under the LAZY policy, K3 (second checksum of flagged layers) -- is
+ * bracketed by CUDA events on the handle's stream (the events also disable
+ * the programmatic-dependent-launch overlap between them).  profile_read
+ * synchronises, returns the summed device time (ms) and launch counts of K1
+ * and of the checks (k2_*) since the last read, and resets them.  Also
+ * reports the K1 launch geometry (grid x, y, z, threads per CTA, dynamic
+ * shared memory bytes, layers per CTA) when geo != NULL. */
 int abft_stencil_profile(abft_stencil* h, int32_t enable);
 int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_launches,
                               double* k2_ms, int64_t* k2_launches, int32_t geo[6]);
