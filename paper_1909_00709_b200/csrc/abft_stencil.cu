@@ -861,10 +861,14 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   const int tiles_x = (int)((nx + h->geo.tile_x - 1) / h->geo.tile_x);
   const int tiles_y = (int)((ny + h->geo.tile_y - 1) / h->geo.tile_y);
   const int64_t tiles = (int64_t)tiles_x * tiles_y;
+  // z-chunks: ~32 waves of resident CTAs (the last, partial wave then costs
+  // little; measured on cfg4: 8 waves / 103 layers per CTA -> 32 waves / 28
+  // layers: protected K1 -3%), but >= 16 layers per CTA (each chunk re-stages
+  // its two z-halo layers)
   const int per_sm = std::max(1, (228 * 1024) / (h->geo.smem + 1024));
-  const int64_t target = (int64_t)8 * nsm * per_sm;
+  const int64_t target = (int64_t)32 * nsm * per_sm;
   int64_t nch = std::max<int64_t>(1, std::min<int64_t>(zc, (target + tiles - 1) / tiles));
-  h->zchunk = (int)((zc + nch - 1) / nch);
+  h->zchunk = (int)std::max<int64_t>((zc + nch - 1) / nch, std::min<int64_t>(zc, 16));
   if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
   h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
 

@@ -44,7 +44,10 @@ __device__ __forceinline__ void bump(DevState* st, int k, long long v = 1) {
   atomicAdd(reinterpret_cast<unsigned long long*>(&st->cnt[k]), (unsigned long long)v);
 }
 
-constexpr int kCheckThreads = 128;   // 10+ CTAs per SM: every layer of a 1024-layer slab in one wave
+#ifndef ABFT_CHECK_THREADS
+#define ABFT_CHECK_THREADS 128
+#endif
+constexpr int kCheckThreads = ABFT_CHECK_THREADS;   // 9+ CTAs per SM: a 1024-layer slab in one wave
 
 // one entry of a'_x (A == true) or b'_y of layer z, Theorem 1 (Eqs. 4-5):
 //   a'_x = c_x + sum_S w (a_{zeta(z+k)}[x+i] + alpha_{x+i, j})
