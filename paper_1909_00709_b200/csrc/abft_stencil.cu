@@ -868,7 +868,12 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   const int per_sm = std::max(1, (228 * 1024) / (h->geo.smem + 1024));
   const int64_t target = (int64_t)32 * nsm * per_sm;
   int64_t nch = std::max<int64_t>(1, std::min<int64_t>(zc, (target + tiles - 1) / tiles));
-  h->zchunk = (int)std::max<int64_t>((zc + nch - 1) / nch, std::min<int64_t>(zc, 16));
+  int64_t zch = std::max<int64_t>((zc + nch - 1) / nch, std::min<int64_t>(zc, 16));
+  // ... unless that leaves SMs idle (few tiles and layers: cfg2), then about
+  // one wave
+  const int64_t slots = (int64_t)nsm * per_sm;
+  if (tiles * ((zc + zch - 1) / zch) < slots) zch = std::max<int64_t>(1, tiles * zc / slots);
+  h->zchunk = (int)zch;
   if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
   h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
 
