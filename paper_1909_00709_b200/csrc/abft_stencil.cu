@@ -223,12 +223,6 @@ struct abft_stencil {
   int field_src = -1;
   cudaStream_t stream = nullptr;
   CUtensorMap tm_u[3];
-  // y-march K1 (3D shapes): (x, z) slice boxes, persistent grid
-  bool ymarch = false;
-  CUtensorMap tm_uy[3];
-  CUtensorMap tm_srcy;
-  K1Geometry geoy;
-  dim3 gridy;
   int shape = SHAPE_GENERIC;
   K1Geometry geo;
   dim3 grid1;
@@ -389,13 +383,7 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
                   : (inj ? K1_INJ : K1_HOT);
   h->executed++;
   cudaEvent_t* pe = prof_begin(h, 1);
-  cudaError_t e;
-  if (h->ymarch)
-    e = h->cfg.dtype == ABFT_F32
-            ? launch_k1y_f32(h->shape, chk == K1_CK_AB, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p)
-            : launch_k1y_f64(h->shape, chk == K1_CK_AB, inj, h->gridy, h->stream, h->tm_uy[src], h->tm_srcy, p);
-  else
-    e = h->cfg.dtype == ABFT_F32
+  const cudaError_t e = h->cfg.dtype == ABFT_F32
             ? launch_k1_f32(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p)
             : launch_k1_f64(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p);
   prof_end(h, pe);
@@ -877,42 +865,10 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
   h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
 
-  // 3D point lists on slabs of >= 16 layers run the y-march K1 (sweep_y.cuh):
-  // a_x accumulates in registers along y, no tail wave.  ABFT_K1_MARCH=z|y
-  // overrides (tests of both traversals).
-  bool needs_z = false;
-  for (int q = 0; q < cfg->npoints; ++q) needs_z |= cfg->points[q].dk != 0;
-  h->ymarch = false;   // measured slower on cfg4 (profiles/r01): opt-in only
-  if (const char* e = getenv("ABFT_K1_MARCH")) {
-    if (e[0] == 'z') h->ymarch = false;
-    if (e[0] == 'y') h->ymarch = needs_z && cfg->checksum_policy == ABFT_CK_BOTH && cfg->bc == ABFT_BC_CLAMP;
-  }
-  int ntx = 0, ntz = 0;
-  if (h->ymarch) {
-    h->geoy = k1y_geometry(cfg->dtype);
-    for (int b = 0; b < h->nbuf; ++b)
-      if (!encode3d(&h->tm_uy[b], cfg->dtype, h->fb[b], nx, ny, zc + 2, L.px * esz, L.plane * esz,
-                    h->geoy.tile_x + 2 * HV, 1, h->geoy.tile_y + 2,
-                    getenv("ABFT_Y_PROMO256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                              : CU_TENSOR_MAP_L2_PROMOTION_NONE))
-        return fail(ABFT_ECUDA);
-    memset(&h->tm_srcy, 0, sizeof(h->tm_srcy));
-    if (h->field_src >= 0 &&
-        !encode3d(&h->tm_srcy, cfg->dtype, const_cast<void*>(h->src_field), nx, ny, zc, h->src_px * esz,
-                  h->src_px * ny * esz, h->geoy.tile_x, 1, h->geoy.tile_y))
-      return fail(ABFT_ECUDA);
-    ntx = (int)((nx + h->geoy.tile_x - 1) / h->geoy.tile_x);
-    ntz = (int)((zc + h->geoy.tile_y - 1) / h->geoy.tile_y);
-    const int occ = cfg->dtype == ABFT_F32 ? k1y_occ_f32(h->shape) : k1y_occ_f64(h->shape);
-    const int64_t rows = (int64_t)ntx * ntz * ny;
-    h->gridy = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)nsm * occ)));
-  }
-
   // parameter blocks (weights and coefficients rounded to the dtype)
   SweepParams& sp = h->sp;
   memset(&sp, 0, sizeof(sp));
   sp.nx = (int)nx; sp.ny = (int)ny; sp.zc = (int)zc; sp.zchunk = h->zchunk;
-  sp.ntx = ntx; sp.ntz = ntz;
   sp.bc = cfg->bc;
   sp.g = cfg->bc == ABFT_BC_CONSTANT ? rnd(cfg->dtype, cfg->bc_value) : 0.0;
   sp.src = h->src_field;
@@ -968,7 +924,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   // load every kernel variant this handle may launch (hot / flip / general K1
   // for each checksum mode, K2, K3) now: with CUDA's lazy module loading the
   // first sweep carrying a flip would otherwise pay the load inside the run
-  if (!h->ymarch) {
+  {
     const int vars[3] = {K1_HOT, K1_INJ, K1_GEN};
     const int chks[3] = {K1_CK_NONE, K1_CK_AB, K1_CK_B};
     for (int ci = 0; ci < 3; ++ci)
@@ -1022,7 +978,6 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
   // device, or a peer GPU with peer access (NVLink); ABFT_GROUP_COPY=1 keeps
   // the device-copy exchange
   bool fused = !(getenv("ABFT_GROUP_COPY") && getenv("ABFT_GROUP_COPY")[0] == '1');
-  for (int i = 0; i < n; ++i) fused = fused && !hs[i]->ymarch;   // the y-march K1 stores locally only
   int cur_dev = 0;
   CK(cudaGetDevice(&cur_dev));
   for (int i = 0; i + 1 < n && fused; ++i) {
@@ -1266,10 +1221,7 @@ int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_n, dou
   if (k1_n) *k1_n = n[1];
   if (k2_ms) *k2_ms = t[2];
   if (k2_n) *k2_n = n[2];
-  if (geo && h->ymarch) {   // persistent y-march: grid, threads, smem, layers per tile
-    geo[0] = h->gridy.x; geo[1] = 1; geo[2] = 1;
-    geo[3] = h->geoy.threads; geo[4] = h->geoy.smem; geo[5] = h->geoy.tile_y;
-  } else if (geo) {
+  if (geo) {
     geo[0] = h->grid1.x; geo[1] = h->grid1.y; geo[2] = h->grid1.z;
     geo[3] = h->geo.threads; geo[4] = h->geo.smem; geo[5] = h->zchunk;
   }

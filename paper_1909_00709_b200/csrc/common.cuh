@@ -51,9 +51,8 @@ template <> struct Shape<SHAPE_BOX27> {
   }
 };
 
-// The helpers take the shape as a type so a kernel can evaluate the same
-// point list with two axes exchanged (SwapYZ: the y-march of sweep_y.cuh
-// stages (x, z) slices and slides along y).
+// The helpers take the shape as a type (a point list seen in staged
+// coordinates).
 template <class SH> __host__ __device__ constexpr bool sh_needs_z() {
   for (int p = 0; p < SH::NP; ++p)
     if (SH::off(p, 2) != 0) return true;
@@ -72,13 +71,6 @@ template <class SH> __host__ __device__ constexpr bool sh_uses_x_halo(int dk) {
 }
 template <int S> __host__ __device__ constexpr bool shape_needs_z() { return sh_needs_z<Shape<S>>(); }
 
-// the point list of shape S with the y and z axes exchanged (same point order)
-template <int S> struct SwapYZ {
-  static constexpr int NP = Shape<S>::NP;
-  __host__ __device__ static constexpr int off(int p, int a) {
-    return Shape<S>::off(p, a == 1 ? 2 : (a == 2 ? 1 : 0));
-  }
-};
 
 // K1 instantiation variants: hot path, with scheduled bit-flips, general
 enum K1Variant { K1_HOT = 0, K1_INJ = 1, K1_GEN = 2 };
@@ -171,7 +163,6 @@ struct CheckParams {
 
 struct SweepParams {
   int nx, ny, zc, zchunk;
-  int ntx, ntz;        // y-march: x-tiles x z-tiles (each ny rows), split over the grid
   int64_t px;          // row pitch of the field buffers (elements)
   int64_t plane;       // layer pitch = px * ny
   int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)

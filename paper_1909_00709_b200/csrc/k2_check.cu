@@ -4,7 +4,6 @@
 #include "check.cuh"
 #include "launch.h"
 #include "sweep.cuh"
-#include "sweep_y.cuh"  // YTile geometry only
 
 namespace abft {
 
@@ -13,10 +12,6 @@ K1Geometry k1_geometry(int dtype) {
   return {Tile<double>::TX, Tile<double>::TY, Tile<double>::SMEM, Tile<double>::THREADS};
 }
 
-K1Geometry k1y_geometry(int dtype) {
-  if (dtype == ABFT_F32) return {YTile<float>::TX, YTile<float>::TZ, YTile<float>::SMEM, YTile<float>::THREADS};
-  return {YTile<double>::TX, YTile<double>::TZ, YTile<double>::SMEM, YTile<double>::THREADS};
-}
 
 template <typename T, bool BCG>
 static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p) {

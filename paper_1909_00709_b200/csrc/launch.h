@@ -31,8 +31,7 @@ struct K1Geometry {
   int tile_x, tile_y, smem, threads;
 };
 K1Geometry k1_geometry(int dtype);
-// y-march (3D shapes): tile_x x tile_y = x-columns x z-layers of one tile
-K1Geometry k1y_geometry(int dtype);
+
 
 cudaError_t launch_k1_f32(int shape, int chk, int var, dim3 grid, cudaStream_t s,
                           const CUtensorMap& tu, const SweepParams& p);
@@ -46,13 +45,6 @@ ABFT_K1_DECL(launch_k1_f32_s3) ABFT_K1_DECL(launch_k1_f32_s4)
 ABFT_K1_DECL(launch_k1_f64_s0) ABFT_K1_DECL(launch_k1_f64_s1) ABFT_K1_DECL(launch_k1_f64_s2)
 ABFT_K1_DECL(launch_k1_f64_s3) ABFT_K1_DECL(launch_k1_f64_s4)
 #undef ABFT_K1_DECL
-cudaError_t launch_k1y_f32(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
-                           const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
-cudaError_t launch_k1y_f64(int shape, bool chk, bool inj, dim3 grid, cudaStream_t s,
-                           const CUtensorMap& tu, const CUtensorMap& ts, const SweepParams& p);
-// resident CTAs per SM of the y-march kernel (occupancy query)
-int k1y_occ_f32(int shape);
-int k1y_occ_f64(int shape);
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
 // fill n elements of a field buffer with v (constant ghost layers)
 cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t s);

@@ -146,8 +146,8 @@ __device__ __forceinline__ void row_sums(const T (&out)[RY][16 / sizeof(T)], dou
 // the shape's point order; srow[t] = staged row of input row (first - 1 + t),
 // already clamped or mapped to a halo.  EDGE: the tile touches
 // x = 0 or x = nx - 1, so out-of-domain x reads take the clamped value.
-// SH is the shape seen in the staged coordinates (Shape<S>, or SwapYZ<S> for
-// the y-march): off(q, 2) selects the plane, off(q, 1) the row.
+// SH is the shape seen in the staged coordinates: off(q, 2) selects the plane,
+// off(q, 1) the row.
 // What an edge tile needs to build the ghosts of Eq. 1 (P:289-292 clamp,
 // P:413-415 periodic / zero / constant): BC, ghost value, the input planes in
 // global memory (periodic wrap reads), the row pitch and the thread's rows.

@@ -21,12 +21,6 @@ def setup_module(module):
         pytest.skip("needs a CUDA device")
 
 
-@pytest.fixture(params=["z", "y"])
-def march(request, monkeypatch):
-    """Both K1 traversals of 3D point lists (sweep.cuh z-march, sweep_y.cuh
-    y-march); the library reads ABFT_K1_MARCH when a handle is created."""
-    monkeypatch.setenv("ABFT_K1_MARCH", request.param)
-    return request.param
 
 
 # ---- BASELINE.json configs at their own size (cfg1, cfg2) ------------------
@@ -54,24 +48,24 @@ def test_cfg2_explicit_api_matches_fused_step():
 
 # ---- reduced cfg3 / cfg5, ragged tiles, degenerate shapes --------------------
 
-def test_cfg3_reduced_online(march):
+def test_cfg3_reduced_online():
     parity(make_problem("cfg3", nz=12, sweeps=60, nfaults=8))
 
 
-def test_cfg3_reduced_offline_rollback(march):
+def test_cfg3_reduced_offline_rollback():
     p = make_problem("cfg3", nz=12, sweeps=60, nfaults=8, mode=2, delta=10)
     g, o = parity(p)
     assert o["stats"]["rollbacks"] >= 1
 
 
-def test_offline_last_window_shorter_than_delta(march):
+def test_offline_last_window_shorter_than_delta():
     p = make_problem("cfg3", nx=128, ny=96, nz=5, sweeps=23, nfaults=4, mode=2, delta=10)
     parity(p)
 
 
 @pytest.mark.parametrize("nx,ny,nz", [(203, 77, 9), (129, 33, 3), (64, 100, 2), (5, 3, 4),
                                       (1, 1, 1), (1, 7, 3), (9, 1, 2), (260, 1, 1)])
-def test_hotspot_ragged_and_degenerate_shapes(nx, ny, nz, march):
+def test_hotspot_ragged_and_degenerate_shapes(nx, ny, nz):
     p = make_problem("cfg2", nx=nx, ny=ny, nz=nz, sweeps=25, nfaults=2)
     faults = [Fault(7, nz - 1, ny - 1, nx - 1, 30), Fault(15, 0, 0, 0, 27)]
     parity(p, faults=faults)
@@ -83,19 +77,19 @@ def test_fig2_five_point_2d(nx, ny):
     parity(p, faults=[Fault(10, 0, ny // 2, nx // 3, 29)])
 
 
-def test_cfg5_reduced_fp64_box27_offline(march):
+def test_cfg5_reduced_fp64_box27_offline():
     p = make_problem("cfg5", nx=130, ny=67, nz=12, sweeps=20, nfaults=6)
     g, o = parity(p)
 
 
-def test_cfg5_reduced_fp64_box27_online(march):
+def test_cfg5_reduced_fp64_box27_online():
     p = make_problem("cfg5", nx=66, ny=40, nz=7, sweeps=15, nfaults=5, mode=1)
     parity(p)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("seed", [0, 1])
-def test_generic_stencil_random_order(dtype, seed, march):
+def test_generic_stencil_random_order(dtype, seed):
     # an arbitrary radius-1 point list in arbitrary order runs the generic kernel
     rng = random.Random(seed)
     offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
@@ -120,7 +114,7 @@ def test_correction_literal_form_runs():
 
 # ---- non-interference: protection does not change the sweep (SPEC #3) -------
 
-def test_protected_field_equals_unprotected_field(march):
+def test_protected_field_equals_unprotected_field():
     p = make_problem("cfg2", nz=6, sweeps=40)
     g1 = gpu_run(p, faults=[])
     g0 = gpu_run(p.replace(mode=0), faults=[])
@@ -235,7 +229,7 @@ def halo(request, monkeypatch):
 
 @pytest.mark.parametrize("G,uneven", [(2, False), (2, True), (3, False), (4, False)])
 @pytest.mark.parametrize("mode", [1, 2])
-def test_slab_group_equals_oracle(G, uneven, mode, march, halo):
+def test_slab_group_equals_oracle(G, uneven, mode, halo):
     # per-layer arithmetic does not depend on the partition, so
     # any z-slab decomposition is bitwise identical to the single domain.
     from tests.parity_util import assert_records_equal
@@ -265,14 +259,15 @@ def test_slab_group_fp64_box27_offline(march, halo):
     assert_records_equal(g, o, exact_values=False, rtol=1e-12)
 
 
-# ---- y-march specifics: persistent segments crossing tiles, tile-edge flips --
+# ---- tiles: several z-chunks and x/y tiles, flips on chunk and tile edges -----
 
 @pytest.mark.parametrize("nx,ny,nz", [(300, 200, 70), (129, 47, 33), (64, 16, 96)])
-def test_ymarch_segments_and_tile_edges(nx, ny, nz, march):
+def test_tile_and_chunk_edges(nx, ny, nz):
     p = make_problem("cfg3", nx=nx, ny=ny, nz=nz, sweeps=16, nfaults=0)
-    zs = sorted({0, 31, 32, min(63, nz - 1), nz - 1})
+    zs = sorted({0, 15, 16, 31, 32, min(63, nz - 1), nz - 1})
     faults = [Fault(2 + i, z, (7 * i) % ny, (37 * i + 127) % nx, 30 - i) for i, z in enumerate(zs)]
     faults += [Fault(9, nz // 2, ny - 1, nx - 1, 29), Fault(12, nz // 3, 0, 128 % nx, 28)]
+    faults = list({(f.sweep, f.z, f.y, f.x): f for f in faults}.values())
     parity(p, faults=faults)
 
 
