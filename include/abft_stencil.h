@@ -208,8 +208,8 @@ int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
  * checksum (or offline prediction) rows and any correction there too --
  * straight to the neighbour's memory (same device, or a peer GPU over NVLink
  * with peer access enabled by group()); events order each slab's next sweep
- * after its neighbours' sweep.  ABFT_GROUP_COPY=1, GPUs without peer access,
- * or the y-march fall back to device copies after each sweep.  step_group() runs n
+ * after its neighbours' sweep.  ABFT_GROUP_COPY=1 or GPUs without peer access
+ * fall back to device copies after each sweep.  step_group() runs n
  * protected sweeps of every slab in lockstep (offline: windows, verdicts and
  * rollbacks are collective).  abft_stencil_step / _sweep / _check / _correct
  * reject grouped handles (ABFT_EINVAL).  Destroying a member dissolves the
