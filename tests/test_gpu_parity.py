@@ -248,7 +248,7 @@ def test_slab_group_equals_oracle(G, uneven, mode, halo):
         assert sum(s[k] for s in g["stats"]) == o["stats"][k]
 
 
-def test_slab_group_fp64_box27_offline(march, halo):
+def test_slab_group_fp64_box27_offline(halo):
     from tests.parity_util import assert_records_equal
     p = make_problem("cfg5", nx=70, ny=33, nz=9, sweeps=15, nfaults=6)
     faults = fault_schedule(p)
