@@ -215,6 +215,12 @@ int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
  * reject grouped handles (ABFT_EINVAL).  Destroying a member dissolves the
  * group. */
 int abft_stencil_group(abft_stencil* const* hs, int32_t n);
+
+/* The z-slab halo plan of cfg (one process per GPU, NCCL): for the lower
+ * (plan[0..2]) and upper (plan[3..5]) face, the peer rank, the buffer layer
+ * sent (1 or z_count) and the halo layer received (0 or z_count + 1); -1
+ * where there is no neighbour.  No device needed. */
+int abft_stencil_halo_plan(const abft_config* cfg, int32_t plan[6]);
 int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps);
 
 /* Explicit-control API (ONLINE / NONE handles), the paper's listings one by

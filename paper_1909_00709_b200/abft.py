@@ -30,7 +30,8 @@ EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_ste
            "abft_stencil_checksums", "abft_stencil_stats", "abft_stencil_records",
            "abft_stencil_status", "abft_stencil_sweep_count", "abft_stencil_launch_count",
            "abft_stencil_destroy", "abft_strerror", "abft_stencil_profile",
-           "abft_stencil_profile_read", "abft_stencil_group", "abft_stencil_step_group")
+           "abft_stencil_profile_read", "abft_stencil_group", "abft_stencil_step_group",
+           "abft_stencil_halo_plan")
 
 
 class abft_point(C.Structure):
@@ -113,6 +114,7 @@ def lib() -> C.CDLL:
         L.abft_stencil_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64),
                                                 C.POINTER(C.c_double), C.POINTER(i64),
                                                 C.POINTER(i32)]
+        L.abft_stencil_halo_plan.argtypes = [cfgp, C.POINTER(i32)]
         L.abft_stencil_group.argtypes = [C.POINTER(vp), i32]
         L.abft_stencil_step_group.argtypes = [C.POINTER(vp), i32, i32]
         L.abft_strerror.argtypes = [C.c_int]
@@ -176,6 +178,13 @@ def make_config(nx: int, ny: int, nz: int, dtype, points: Sequence[Tuple[int, in
         idbuf = C.create_string_buffer(bytes(nccl_unique_id), 128)
         c.nccl_unique_id = C.cast(idbuf, C.c_void_p)
     return c, (pts, srcs, idbuf)
+
+
+def abft_stencil_halo_plan(cfg: abft_config) -> List[Tuple[int, int, int]]:
+    """[(peer, send_layer, recv_layer)] per face that has a neighbour, lower first."""
+    plan = (C.c_int32 * 6)()
+    _ok("abft_stencil_halo_plan", lib().abft_stencil_halo_plan(C.byref(cfg), plan))
+    return [(plan[3 * f], plan[3 * f + 1], plan[3 * f + 2]) for f in (0, 1) if plan[3 * f] >= 0]
 
 
 def abft_stencil_workspace_size(cfg: abft_config) -> Tuple[int, int]:

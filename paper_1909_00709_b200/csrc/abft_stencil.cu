@@ -445,6 +445,19 @@ void xvecs(abft_stencil* h, const XSpec& x, double** a, double** b) {
 }
 
 // NCCL transport (one process per GPU): send / recv to rank -+ 1 in one group
+// the z-slab halo plan of (rank, nranks, z_count): per face (0 = lower,
+// 1 = upper) the peer rank, the buffer layer sent and the halo layer received
+// (-1 when there is no neighbour) -- the plan paper_1909_00709_b200/dist.py
+// states and tests with gloo
+void halo_plan(const abft_config& c, int32_t plan[6]) {
+  for (int side = 0; side < 2; ++side) {
+    const bool has = side == 0 ? c.rank > 0 : c.rank < c.nranks - 1;
+    plan[3 * side + 0] = has ? c.rank + (side == 0 ? -1 : 1) : -1;
+    plan[3 * side + 1] = has ? (side == 0 ? 1 : (int32_t)c.z_count) : -1;
+    plan[3 * side + 2] = has ? (side == 0 ? 0 : (int32_t)c.z_count + 1) : -1;
+  }
+}
+
 int exchange_nccl(abft_stencil* h, const XSpec& x) {
   NcclApi* n = nccl_api();
   if (!n) return ABFT_ENCCL;
@@ -455,12 +468,14 @@ int exchange_nccl(abft_stencil* h, const XSpec& x) {
   double *va, *vb;
   xvecs(h, x, &va, &vb);
   const std::pair<double*, int64_t> vecs[2] = {{va, h->cfg.nx}, {vb, h->cfg.ny}};
+  int32_t plan[6];
+  halo_plan(h->cfg, plan);
+  (void)zc;
   if (n->groupStart() != ncclSuccess) return ABFT_ENCCL;
   for (int side = 0; side < 2; ++side) {
-    const bool has = side == 0 ? h->has_lo : h->has_hi;
-    if (!has) continue;
-    const int peer = h->cfg.rank + (side == 0 ? -1 : 1);
-    const int64_t send_l = side == 0 ? 1 : zc, recv_l = side == 0 ? 0 : zc + 1;
+    const int peer = plan[3 * side];
+    if (peer < 0) continue;
+    const int64_t send_l = plan[3 * side + 1], recv_l = plan[3 * side + 2];
     n->send(buf + send_l * lb * esz, lb, dt, peer, h->comm, h->stream);
     n->recv(buf + recv_l * lb * esz, lb, dt, peer, h->comm, h->stream);
     for (const auto& v : vecs) {
@@ -728,6 +743,14 @@ int step_group(Group& G, int32_t n) {
 
 // =================================================================== C-ABI
 extern "C" {
+
+int abft_stencil_halo_plan(const abft_config* cfg, int32_t plan[6]) {
+  if (!plan) return ABFT_EINVAL;
+  const int v = validate(cfg);
+  if (v) return v;
+  halo_plan(*cfg, plan);
+  return ABFT_OK;
+}
 
 const char* abft_strerror(int s) {
   switch (s) {

@@ -109,6 +109,18 @@ def test_multi_rank_slab_config_accepted(L):
     assert fb >= 64 * 32 * 4 * 4
 
 
+@pytest.mark.parametrize("nz,world", [(4, 1), (4, 2), (7, 3), (9, 4), (16, 8)])
+def test_library_halo_plan_matches_dist(L, nz, world):
+    """The library's NCCL exchange plan (abft_stencil_halo_plan, used by
+    exchange_nccl) equals the host plan dist.halo_plan that the gloo tests run."""
+    from paper_1909_00709_b200 import dist
+    for rank in range(world):
+        z0, zc = dist.slab(nz, world, rank)
+        c, keep = _cfg(nz=nz, nranks=world, rank=rank, z_begin=z0, z_count=zc,
+                       nccl_unique_id=b"\0" * 128 if world > 1 else None)
+        assert abft.abft_stencil_halo_plan(c) == dist.halo_plan(rank, world, zc)
+
+
 def test_stencil_refuses_cpu_device(L):
     import torch
     c, keep = _cfg()
