@@ -355,6 +355,52 @@ static int32_t check_layer(const or_problem* p, int64_t s, int64_t z, void* u, c
     push(recs, cap, nrec, &r);
     return 0;
   }
+  if (p->correction_form == 2) {
+    /* form 2 when the flags do not intersect in one cell (several flagged
+       entries, or only one vector flagged): stencil locality (P:107-108,
+       P:743-745) -- u^(t) is intact, so every cell of layer z is recomputed
+       from it with Eq. 1 and the cells whose stored value differs (bitwise)
+       are the errors; they are rewritten, and a[z], b[z] are re-summed from
+       the repaired layer (Eqs. 2-3, ascending index order).  Reading Q27. */
+    int64_t changed = 0;
+    for (int64_t y = 0; y < ny; y++)
+      for (int64_t x = 0; x < nx; x++) {
+        const int64_t c = (z * ny + y) * nx + x;
+        const double v = cell_update(p, uprev, z, y, x);
+        int differs;
+        if (p->dtype == OR_F32) {
+          const float fv = (float)v;
+          differs = memcmp(&fv, (const float*)u + c, sizeof fv) != 0;
+        } else {
+          differs = memcmp(&v, (const double*)u + c, sizeof v) != 0;
+        }
+        if (!differs) continue;
+        or_record rc = r;
+        rc.y = y; rc.x = x;
+        rc.observed = ld(u, c, p->dtype); rc.corrected = v;
+        rc.status = OR_REC_RECOMPUTED;
+        st(u, c, p->dtype, v);
+        st_->located++;
+        st_->corrected++;
+        push(recs, cap, nrec, &rc);
+        changed++;
+      }
+    for (int64_t x = 0; x < nx; x++) {
+      double a = 0.0;
+      for (int64_t y = 0; y < ny; y++) a += ld(u, (z * ny + y) * nx + x, p->dtype);
+      A[z * nx + x] = a;
+    }
+    for (int64_t y = 0; y < ny; y++) {
+      double b = 0.0;
+      for (int64_t x = 0; x < nx; x++) b += ld(u, (z * ny + y) * nx + x, p->dtype);
+      B[z * ny + y] = b;
+    }
+    if (changed == 0) {
+      r.status = OR_REC_VERIFIED;
+      push(recs, cap, nrec, &r);
+    }
+    return 0;
+  }
   if (na == 0 || nb == 0) {
     r.status = OR_REC_UNLOCATED;         /* fig.abft.error scenario 2, Q14 */
     st_->unlocated++;

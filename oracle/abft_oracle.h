@@ -30,7 +30,11 @@ enum {
   OR_REC_UNLOCATED = 2,      /* only one checksum vector flagged        */
   OR_REC_UNCORRECTABLE = 3,  /* >= 2 flags in a vector of one plane (Q13)       */
   OR_REC_WINDOW_DIRTY = 4,   /* offline: plane flagged at window end    */
-  OR_REC_PERSISTENT = 5      /* offline: still flagged after rollback           */
+  OR_REC_PERSISTENT = 5,     /* offline: still flagged after rollback           */
+  OR_REC_RECOMPUTED = 6,     /* form 2, no single intersection: the layer was
+                                recomputed from u^(t) and this cell differed  */
+  OR_REC_VERIFIED = 7        /* form 2, no single intersection: the layer was
+                                recomputed and no cell differed               */
 };
 
 typedef struct { int32_t di, dj, dk, pad; double w; } or_point;

@@ -459,6 +459,52 @@ def test_correction_by_recompute_restores_the_fault_free_run(name, kw):
     assert done >= 15
 
 
+@pytest.mark.parametrize("cells", [
+    ((7, 9), (20, 31)),            # two rows, two columns: 2x2 flagged, no single intersection
+    ((7, 9), (7, 31)),             # one row, two columns
+    ((7, 9), (20, 9), (33, 2)),    # one column twice + a third cell
+])
+@pytest.mark.parametrize("checksums", [0, 1])
+def test_recompute_repairs_several_flips_in_one_layer(cells, checksums):
+    # correction_form 2 when the flags do not intersect in one cell (Q27):
+    # recomputing layer z from the intact u^(t) (locality)
+    # finds exactly the flipped cells, restores the fault-free field bitwise,
+    # and the re-summed a, b are the exact column / row sums (Eqs. 2-3; fp32
+    # HotSpot data sum exactly in fp64).  Forms 0 / 1 leave such a layer
+    # "uncorrectable" / "unlocated" (Q13, Q14).
+    p = make_problem("cfg2", nx=40, ny=36, nz=4, sweeps=6, checksums=checksums)
+    op = O.OProblem(p, [field_power(p).numpy()])
+    u0 = field_u0(p).numpy()
+    ref = O.run(op, u0, p.sweeps)
+    faults = [Fault(4, 2, y, x, 29) for y, x in cells]
+    r0 = O.run(op, u0, p.sweeps, faults)
+    assert r0["stats"]["corrected"] == 0 and r0["stats"]["uncorrectable"] + r0["stats"]["unlocated"] == 1
+    p2 = p.replace(correction_form=2)
+    r = O.run(O.OProblem(p2, [field_power(p2).numpy()]), u0, p.sweeps, faults)
+    assert (r["u"].view(np.uint32) == ref["u"].view(np.uint32)).all()
+    rec = [(x["sweep"], x["z"], x["y"], x["x"]) for x in r["records"]]
+    assert sorted(rec) == sorted((4, 2, y, x) for y, x in cells)
+    assert all(x["status"] == O.REC_RECOMPUTED for x in r["records"])
+    assert r["stats"]["detections"] == 1 and r["stats"]["corrected"] == len(cells)
+    u = r["u"].astype(np.float64)
+    assert np.array_equal(r["A"], u.sum(axis=1)) and np.array_equal(r["B"], u.sum(axis=2))
+
+
+def test_recompute_false_alarm_leaves_the_field():
+    # a threshold far below the prediction's rounding error flags error-free
+    # layers; form 2 recomputes them, finds no differing cell ("verified") and
+    # the field is the fault-free run's, bitwise.
+    p = make_problem("cfg5", nx=20, ny=17, nz=4, sweeps=5, mode=1, nfaults=0)
+    op = O.OProblem(p)
+    u0 = field_u0(p).numpy()
+    ref = O.run(op, u0, p.sweeps, [])
+    tight = p.replace(correction_form=2, eps=1e-19)
+    r = O.run(O.OProblem(tight), u0, p.sweeps, [])
+    assert r["stats"]["detections"] > 0 and r["stats"]["corrected"] == 0
+    assert r["records"] and all(x["status"] == O.REC_VERIFIED for x in r["records"])
+    assert (r["u"].view(np.uint64) == ref["u"].view(np.uint64)).all()
+
+
 def test_correction_literal_form_fails_on_exponent_flip():
     # "if the bit-flips occur in the last bits of the exponent, the error
     # causes an overflow in the checksums" -- the literal fig.correction form
