@@ -86,7 +86,12 @@ typedef enum {
   ABFT_REC_UNLOCATED = 2,     /* only one checksum vector flagged        */
   ABFT_REC_UNCORRECTABLE = 3, /* >= 2 flagged entries in a vector of one layer    */
   ABFT_REC_WINDOW_DIRTY = 4,  /* offline: layer flagged at a window end   */
-  ABFT_REC_PERSISTENT = 5     /* offline: layer still flagged after the rollback  */
+  ABFT_REC_PERSISTENT = 5,    /* offline: layer still flagged after the rollback  */
+  ABFT_REC_RECOMPUTED = 6,    /* correction_form 2, flags not intersecting in one
+                                 cell: the layer was recomputed from u^{s-1} and
+                                 this cell differed (rewritten)                  */
+  ABFT_REC_VERIFIED = 7       /* correction_form 2, flags not intersecting in one
+                                 cell: the layer was recomputed, no cell differed */
 } abft_record_status;
 
 /* ---- problem statement ---------------------------------------------------- */
@@ -128,7 +133,11 @@ typedef struct {
   int32_t correction_form; /* 0: Eq. 8 with (a - u) re-summed over the other cells
                               (default); 1: literal fig.correction listing; 2: the
                               located cell recomputed from u^{s-1} with Eq. 1
-                              (stencil locality: exact repair) */
+                              (stencil locality: exact
+                              repair); when the flags do not intersect in one
+                              cell, the whole layer is recomputed, the differing
+                              cells rewritten and a, b of the layer re-summed
+                              (Q27) */
   int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
   int32_t checksum_policy; /* abft_checksum_policy (ONLINE step() only) */
   const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by
@@ -186,7 +195,10 @@ int abft_stencil_workspace_size(const abft_config* cfg, size_t* field_bytes, siz
  * stream: cudaStream_t to run on (NULL = default stream).  Computes the
  * trusted initial checksums a^0, b^0 and c_x, c_y, and (nranks > 1) creates
  * the NCCL communicator and exchanges the initial halo.  Asynchronous on
- * `stream` except for NCCL initialisation. */
+ * `stream` except for NCCL initialisation.  Ordering is the caller's: u0,
+ * the source fields and the buffers must be ready for work on `stream` (a
+ * producer on another stream is waited for first), and stay allocated until
+ * destroy() (which synchronises `stream`). */
 int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* aux,
                       const void* u0, void* stream, abft_stencil** out);
 

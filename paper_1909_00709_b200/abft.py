@@ -22,7 +22,7 @@ ABFT_F32, ABFT_F64 = 0, 1
 ABFT_BC_CLAMP, ABFT_BC_PERIODIC, ABFT_BC_ZERO, ABFT_BC_CONSTANT = 0, 1, 2, 3
 ABFT_MODE_NONE, ABFT_MODE_ONLINE, ABFT_MODE_OFFLINE = 0, 1, 2
 ABFT_CK_BOTH, ABFT_CK_LAZY = 0, 1
-REC_CORRECTED, REC_UNLOCATED, REC_UNCORRECTABLE, REC_WINDOW_DIRTY, REC_PERSISTENT = 1, 2, 3, 4, 5
+REC_CORRECTED, REC_UNLOCATED, REC_UNCORRECTABLE, REC_WINDOW_DIRTY, REC_PERSISTENT, REC_RECOMPUTED, REC_VERIFIED = 1, 2, 3, 4, 5, 6, 7
 
 EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_step",
            "abft_stencil_sweep", "abft_stencil_check", "abft_stencil_correct",
@@ -217,6 +217,14 @@ class Stencil:
         if tuple(u0.shape) != self.shape or u0.dtype != self.dtype:
             raise ValueError(f"u0 must be {self.shape} {self.dtype}")
         self._u0 = u0.contiguous()
+        # u0 and the source fields may still be in flight on any torch stream
+        # (init is not a hot path): the handle's stream starts after them; the
+        # allocator keeps the buffers until the handle's stream is done
+        torch.cuda.synchronize(self.device)
+        cur = torch.cuda.current_stream(self.device)
+        if self.stream != cur:
+            for t in self.fields + [self.aux] + ([self._u0] if self._u0.is_cuda else []):
+                t.record_stream(self.stream)
         bufs = (C.c_void_p * 3)(*([t.data_ptr() for t in self.fields] + [None] * (3 - nbuf)))
         h = C.c_void_p()
         _ok("abft_stencil_init",
@@ -363,4 +371,6 @@ def from_problem(p, u0: torch.Tensor, power: Optional[torch.Tensor] = None, devi
     cfg, keep = problem_config(p, power, **kw)
     st = Stencil(cfg, keep, u0, device=device, stream=stream)
     st._power = power
+    if power is not None and power.is_cuda and st.stream != torch.cuda.current_stream(st.device):
+        power.record_stream(st.stream)   # read by every sweep on the handle's stream
     return st

@@ -161,6 +161,73 @@ __device__ T cell_update(const CheckParams& p, int z, int y, int x) {
   return acc;
 }
 
+__device__ __forceinline__ bool same_bits(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+__device__ __forceinline__ bool same_bits(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// correction_form 2 when the flags of layer z do not intersect in one cell
+// (Q27; locality): every cell of the layer is
+// recomputed from the intact u^{s-1} (Eq. 1, the sweep's own FMA chain, so an
+// intact cell reproduces its stored bits), the differing cells are rewritten
+// and recorded, then a[z] (one thread per column) and b[z] (one thread per
+// row) are re-summed from the repaired layer in ascending index order.  Rare
+// (a detection that Eq. 8 cannot resolve), so one CTA does the layer.
+template <typename T>
+__device__ __noinline__ void recompute_layer(const CheckParams& p, int z, abft_record r) {
+  __shared__ int s_changed;
+  const int tid = threadIdx.x, bz = z + 1, nx = p.nx, ny = p.ny, zc = p.zc;
+  T* lay = reinterpret_cast<T*>(p.ucur) + (size_t)bz * p.plane;
+  if (tid == 0) s_changed = 0;
+  __syncthreads();
+  for (int x = tid; x < nx; x += kCheckThreads) {
+    double a = 0.0;
+    for (int y = 0; y < ny; ++y) {
+      T* cell = lay + (size_t)y * p.px + x;
+      const T v = cell_update<T>(p, z, y, x), uo = *cell;
+      if (!same_bits(v, uo)) {
+        *cell = v;
+        for (int f = 0; f < 2; ++f)   // fused halo: the neighbour's copy
+          if (z == (f == 0 ? 0 : zc - 1) && p.peerU[f])
+            reinterpret_cast<T*>(p.peerU[f])[(size_t)y * p.px + x] = v;
+        if (p.EXc) {
+          T* exc = reinterpret_cast<T*>(p.EXc);
+          if (x == 0) exc[(size_t)bz * ny + y] = v;
+          if (x == nx - 1) exc[(size_t)(zc + 2) * ny + (size_t)bz * ny + y] = v;
+        }
+        abft_record rc = r;
+        rc.y = y; rc.x = x;
+        rc.observed = (double)uo; rc.corrected = (double)v;
+        rc.status = ABFT_REC_RECOMPUTED;
+        push_record(p.st, rc);
+        bump(p.st, ST_LOCATED); bump(p.st, ST_CORRECTED);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->ncorr), 1ull);
+        atomicAdd(&s_changed, 1);
+      }
+      a += (double)v;
+    }
+    p.Ac[(size_t)bz * nx + x] = a;
+    for (int f = 0; f < 2; ++f)
+      if (z == (f == 0 ? 0 : zc - 1) && p.fwdA[f]) p.fwdA[f][x] = a;
+  }
+  __syncthreads();   // the repaired layer is in place
+  for (int y = tid; y < ny; y += kCheckThreads) {
+    const T* row = lay + (size_t)y * p.px;
+    double b = 0.0;
+    for (int x = 0; x < nx; ++x) b += (double)row[x];
+    p.Bc[(size_t)bz * ny + y] = b;
+    for (int f = 0; f < 2; ++f)
+      if (z == (f == 0 ? 0 : zc - 1) && p.fwdB[f]) p.fwdB[f][y] = b;
+  }
+  if (tid == 0) {
+    bump(p.st, ST_DETECT);
+    if (s_changed == 0) {
+      r.status = ABFT_REC_VERIFIED;
+      push_record(p.st, r);
+    }
+  }
+}
+
 // Steps (4)-(5) for layer z once its compare is complete (na / nb flagged
 // entries, x0 / y0 the first flagged index, pa / pb their predictions); run by
 // every thread of one CTA of kCheckThreads threads (block-uniform arguments).
@@ -235,6 +302,8 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
       bump(p.st, ST_DETECT); bump(p.st, ST_LOCATED); bump(p.st, ST_CORRECTED);
       atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->ncorr), 1ull);
     }
+  } else if (p.form == 2) {
+    recompute_layer<T>(p, z, r);
   } else if (tid == 0) {
     r.status = (na == 0 || nb == 0) ? ABFT_REC_UNLOCATED : ABFT_REC_UNCORRECTABLE;
     push_record(p.st, r);

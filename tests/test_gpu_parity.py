@@ -430,3 +430,45 @@ def test_recompute_correction(name, kw):
     if g["stats"]["corrected"] == len(faults):     # every flip located: exact repair
         w = np.uint32 if p.dtype == "f32" else np.uint64
         assert np.array_equal(g["u"].view(w), ref["u"].view(w))
+
+
+# ---- correction_form 2 beyond one intersection: layer recompute (Q27)
+
+from paper_1909_00709_b200 import abft  # noqa: E402
+
+@pytest.mark.parametrize("cells", [((7, 9), (20, 31)), ((7, 9), (7, 31)), ((7, 9), (20, 9), (33, 2)),
+                                   ((0, 0), (35, 39))])
+@pytest.mark.parametrize("checksums", [0, 1])
+def test_recompute_layer_several_flips(cells, checksums):
+    p = make_problem("cfg2", nx=40, ny=36, nz=4, sweeps=6, checksums=checksums, correction_form=2)
+    faults = [Fault(4, z, y, x, 29) for z in (0, 3) for y, x in cells]
+    g, o = parity(p, faults=faults)
+    assert g["stats"]["corrected"] == len(faults)
+    assert all(r["status"] == abft.REC_RECOMPUTED for r in g["records"])
+    ref = gpu_run(p, faults=[])
+    assert np.array_equal(g["u"].view(np.uint32), ref["u"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("cfg2", dict(nx=203, ny=77, nz=9, sweeps=8)),
+    ("cfg5", dict(nx=40, ny=24, nz=6, sweeps=6, mode=1)),
+])
+def test_recompute_layer_ragged(name, kw):
+    # ragged tiles, several layers at once (one K2 CTA each), fp64 included
+    p = make_problem(name, **kw).replace(correction_form=2)
+    hi = 29 if p.dtype == "f32" else 61
+    faults = [Fault(3, 1, 2, 5, hi), Fault(3, 1, 2, p.nx - 1, hi), Fault(3, 4, 0, 0, hi),
+              Fault(3, 4, p.ny - 1, p.nx - 1, hi), Fault(5, p.nz - 1, 3, 3, hi), Fault(5, p.nz - 1, 9, 17, hi)]
+    g, o = parity(p, faults=faults)
+    assert g["stats"]["corrected"] == len(faults)
+
+
+def test_recompute_false_alarm_verified():
+    # eps far below the prediction's rounding: error-free layers flag; the
+    # recompute finds nothing to rewrite and the field is the fault-free run's
+    p = make_problem("cfg5", nx=40, ny=24, nz=6, sweeps=5, mode=1, nfaults=0)
+    ref = gpu_run(p, faults=[])
+    g = gpu_run(p.replace(correction_form=2, eps=1e-19), faults=[])
+    assert g["stats"]["detections"] > 0 and g["stats"]["corrected"] == 0
+    assert g["records"] and all(r["status"] == abft.REC_VERIFIED for r in g["records"])
+    assert np.array_equal(g["u"].view(np.uint64), ref["u"].view(np.uint64))
