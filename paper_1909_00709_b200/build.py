@@ -43,7 +43,9 @@ def _sources():
     # heaviest translation units first (the K1 instantiations), so the
     # parallel build's critical path is as short as possible
     srcs = glob.glob(os.path.join(CSRC, "*.cu"))
-    return sorted(srcs, key=lambda f: (not os.path.basename(f).startswith("k1"), f))
+    return sorted(srcs, key=lambda f: ("_s3_" not in os.path.basename(f),
+                                       not os.path.basename(f).startswith("k2"),
+                                       not os.path.basename(f).startswith("k1"), f))
 
 
 def _deps():

@@ -1,0 +1,7 @@
+// z-march K1 for float fields, shape SHAPE_BOX27, checksum variant K1_CK_AB only
+// (the 27-point box is the slowest to compile: one unit per variant, built in parallel).
+#define K1_T float
+#define K1_S SHAPE_BOX27
+#define K1_CHK K1_CK_AB
+#define K1_FN launch_k1_f32_s3_ck1
+#include "k1_shape.inc"

@@ -41,9 +41,12 @@ cudaError_t launch_k1_f64(int shape, int chk, int var, dim3 grid, cudaStream_t s
 #define ABFT_K1_DECL(name) \
   cudaError_t name(int chk, int var, dim3 grid, cudaStream_t s, const CUtensorMap& tu, const SweepParams& p);
 ABFT_K1_DECL(launch_k1_f32_s0) ABFT_K1_DECL(launch_k1_f32_s1) ABFT_K1_DECL(launch_k1_f32_s2)
-ABFT_K1_DECL(launch_k1_f32_s3) ABFT_K1_DECL(launch_k1_f32_s4)
+ABFT_K1_DECL(launch_k1_f32_s4)
 ABFT_K1_DECL(launch_k1_f64_s0) ABFT_K1_DECL(launch_k1_f64_s1) ABFT_K1_DECL(launch_k1_f64_s2)
-ABFT_K1_DECL(launch_k1_f64_s3) ABFT_K1_DECL(launch_k1_f64_s4)
+ABFT_K1_DECL(launch_k1_f64_s4)
+// the 27-point box compiles slowest: one translation unit per checksum variant
+ABFT_K1_DECL(launch_k1_f32_s3_ck0) ABFT_K1_DECL(launch_k1_f32_s3_ck1) ABFT_K1_DECL(launch_k1_f32_s3_ck2)
+ABFT_K1_DECL(launch_k1_f64_s3_ck0) ABFT_K1_DECL(launch_k1_f64_s3_ck1) ABFT_K1_DECL(launch_k1_f64_s3_ck2)
 #undef ABFT_K1_DECL
 cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
 // fill n elements of a field buffer with v (constant ghost layers)
