@@ -472,3 +472,16 @@ def test_recompute_false_alarm_verified():
     assert g["stats"]["detections"] > 0 and g["stats"]["corrected"] == 0
     assert g["records"] and all(r["status"] == abft.REC_VERIFIED for r in g["records"])
     assert np.array_equal(g["u"].view(np.uint64), ref["u"].view(np.uint64))
+
+
+def test_recompute_layer_explicit_api():
+    # sweep() / check() / correct() (CK_SUMMARY then CK_FROM_SUMMARY) reach the
+    # same layer recompute as step()
+    p = make_problem("cfg2", nx=72, ny=40, nz=5, sweeps=6, correction_form=2)
+    faults = [Fault(2, 1, 3, 4, 29), Fault(2, 1, 30, 60, 28), Fault(4, 4, 7, 7, 30), Fault(4, 4, 7, 50, 29)]
+    o = oracle_run(p, faults=faults)
+    g = gpu_run(p, faults=faults, explicit=True)
+    assert_field_equal(g, o, "f32")
+    assert sorted((r["sweep"], r["z"], r["y"], r["x"], r["status"]) for r in g["records"]) == \
+        sorted((r["sweep"], r["z"], r["y"], r["x"], r["status"]) for r in o["records"])
+    assert g["stats"]["corrected"] == len(faults)
