@@ -227,10 +227,13 @@ class Stencil:
                 t.record_stream(self.stream)
         bufs = (C.c_void_p * 3)(*([t.data_ptr() for t in self.fields] + [None] * (3 - nbuf)))
         h = C.c_void_p()
-        _ok("abft_stencil_init",
-            lib().abft_stencil_init(C.byref(cfg), bufs, C.c_void_p(self.aux.data_ptr()),
-                                    C.c_void_p(self._u0.data_ptr()),
-                                    C.c_void_p(self.stream.cuda_stream), C.byref(h)))
+        # the library binds the handle to the current device (every later call
+        # runs on that device, whatever is current then)
+        with torch.cuda.device(self.device):
+            _ok("abft_stencil_init",
+                lib().abft_stencil_init(C.byref(cfg), bufs, C.c_void_p(self.aux.data_ptr()),
+                                        C.c_void_p(self._u0.data_ptr()),
+                                        C.c_void_p(self.stream.cuda_stream), C.byref(h)))
         self.h = h
         self._faults = None
 

@@ -265,6 +265,22 @@ struct abft_stencil {
 
 namespace {
 
+// Every per-handle CUDA call runs on the handle's device (a local group may
+// span peer GPUs); the C-ABI entry points restore the caller's device.
+inline void on_dev(const abft_stencil* h) {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess || d != h->dev) cudaSetDevice(h->dev);
+}
+struct DevScope {
+  int old = -1;
+  explicit DevScope(const abft_stencil* h) {
+    if (cudaGetDevice(&old) != cudaSuccess) old = -1;
+    if (h && old != h->dev) cudaSetDevice(h->dev);
+    else old = -1;
+  }
+  ~DevScope() { if (old >= 0) cudaSetDevice(old); }
+};
+
 cudaEvent_t* prof_begin(abft_stencil* h, int kind) {
   if (!h->prof) return nullptr;
   if (h->ev_used * 2 + 2 > h->ev.size()) {
@@ -379,6 +395,7 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
   // K1 variant: constant / periodic ghosts need the general one; scheduled
   // flips the injecting one; everything else runs the hot path
   const bool inj = p.nfaults > 0;
+  on_dev(h);
   const int var = (h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC) ? K1_GEN
                   : (inj ? K1_INJ : K1_HOT);
   h->executed++;
@@ -394,6 +411,7 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
 
 // K2: steps (2)-(5) as their own launch
 int launch_check(abft_stencil* h, const CheckParams& p) {
+  on_dev(h);
   cudaEvent_t* pe = prof_begin(h, 2);
   cudaError_t e = launch_k2(h->cfg.dtype, h->shape, (int)h->cfg.z_count, h->stream, p);
   prof_end(h, pe);
@@ -404,6 +422,7 @@ int launch_check(abft_stencil* h, const CheckParams& p) {
 
 // K3 (lazy policy): a vectors + locate / correct of the layers K2 handed over
 int launch_lazy(abft_stencil* h, const CheckParams& p) {
+  on_dev(h);
   cudaEvent_t* pe = prof_begin(h, 2);
   cudaError_t e = launch_k3(h->cfg.dtype, h->shape, h->stream, p);
   prof_end(h, pe);
@@ -462,7 +481,6 @@ int exchange_nccl(abft_stencil* h, const XSpec& x) {
   NcclApi* n = nccl_api();
   if (!n) return ABFT_ENCCL;
   const ncclDataType_t dt = h->cfg.dtype == ABFT_F32 ? ncclFloat32 : ncclFloat64;
-  const int64_t zc = h->cfg.z_count;
   const size_t lb = (size_t)h->L.plane, esz = h->L.esz;
   char* buf = h->fb[x.buf];
   double *va, *vb;
@@ -470,7 +488,6 @@ int exchange_nccl(abft_stencil* h, const XSpec& x) {
   const std::pair<double*, int64_t> vecs[2] = {{va, h->cfg.nx}, {vb, h->cfg.ny}};
   int32_t plan[6];
   halo_plan(h->cfg, plan);
-  (void)zc;
   if (n->groupStart() != ncclSuccess) return ABFT_ENCCL;
   for (int side = 0; side < 2; ++side) {
     const int peer = plan[3 * side];
@@ -492,8 +509,9 @@ int exchange_nccl(abft_stencil* h, const XSpec& x) {
 // every handle pulls its two halo layers from its neighbours with device
 // copies, ordered by events across the handles' streams.
 int exchange_local(Group& G, const XSpec& x) {
-  for (abft_stencil* h : G) CK(cudaEventRecord(h->ev_ready, h->stream));
+  for (abft_stencil* h : G) { on_dev(h); CK(cudaEventRecord(h->ev_ready, h->stream)); }
   for (abft_stencil* h : G) {
+    on_dev(h);
     const size_t lb = (size_t)h->L.plane * h->L.esz;
     for (int side = 0; side < 2; ++side) {
       abft_stencil* q = side == 0 ? h->lo_peer : h->hi_peer;
@@ -515,19 +533,23 @@ int exchange_local(Group& G, const XSpec& x) {
     CK(cudaEventRecord(h->ev_pulled, h->stream));
   }
   // a neighbour may overwrite the layers we pulled only after our copies ran
-  for (abft_stencil* h : G)
+  for (abft_stencil* h : G) {
+    on_dev(h);
     for (abft_stencil* q : {h->lo_peer, h->hi_peer})
       if (q) CK(cudaStreamWaitEvent(h->stream, q->ev_pulled, 0));
+  }
   return ABFT_OK;
 }
 
 // fused halo: the kernels already wrote every neighbour's halo; order the next
 // sweep of each slab after this sweep of its neighbours
 int sync_local(Group& G) {
-  for (abft_stencil* h : G) CK(cudaEventRecord(h->ev_ready, h->stream));
-  for (abft_stencil* h : G)
+  for (abft_stencil* h : G) { on_dev(h); CK(cudaEventRecord(h->ev_ready, h->stream)); }
+  for (abft_stencil* h : G) {
+    on_dev(h);
     for (abft_stencil* q : {h->lo_peer, h->hi_peer})
       if (q) CK(cudaStreamWaitEvent(h->stream, q->ev_ready, 0));
+  }
   return ABFT_OK;
 }
 
@@ -555,6 +577,7 @@ int halo_exchange(Group& G, const XSpec& x) {
 // halo rows belong to the neighbours' exchange (a fused neighbour may already
 // have written them on its own stream)
 int zero_gen(abft_stencil* h, int g) {
+  on_dev(h);
   const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
   CK(cudaMemsetAsync(h->gA[g] + nx, 0, sizeof(double) * zc * nx, h->stream));
   CK(cudaMemsetAsync(h->gB[g] + ny, 0, sizeof(double) * zc * ny, h->stream));
@@ -625,6 +648,7 @@ int none_sweep(Group& G) {
 int read_dirty(Group& G, int* dirty) {
   *dirty = 0;
   for (abft_stencil* h : G) {
+    on_dev(h);
     if (G.size() == 1 && h->cfg.nranks > 1) {
       NcclApi* n = nccl_api();
       if (!n) return ABFT_ENCCL;
@@ -656,7 +680,7 @@ int offline_window(Group& G, int L) {
   int last = ck;
   int worst = ABFT_OK;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    for (abft_stencil* h : G) CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream));
+    for (abft_stencil* h : G) { on_dev(h); CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream)); }
     int src = ck;
     for (int t = 1; t <= L; ++t) {
       const int64_t s = s0 + t;
@@ -712,6 +736,7 @@ int offline_window(Group& G, int L) {
 
 int clear_summaries(abft_stencil* h) {
   if (h->summ_dirty) {
+    on_dev(h);
     CK(cudaMemsetAsync(h->summ, 0, sizeof(LayerSummary) * h->cfg.z_count, h->stream));
     h->summ_dirty = false;
   }
@@ -984,19 +1009,44 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   return ABFT_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// the members of a group (or the ranks of a job) state the same problem: grid,
+// dtype, stencil S and C (Eq. 1), boundary, threshold, mode, period, policy
+bool same_problem(const abft_config& a, const abft_config& b) {
+  if (a.nx != b.nx || a.ny != b.ny || a.nz_global != b.nz_global || a.dtype != b.dtype ||
+      a.mode != b.mode || a.delta != b.delta || a.npoints != b.npoints || a.nsources != b.nsources ||
+      a.bc != b.bc || a.epsilon != b.epsilon || a.correction_form != b.correction_form ||
+      a.checksum_policy != b.checksum_policy)
+    return false;
+  if (a.bc == ABFT_BC_CONSTANT && a.bc_value != b.bc_value) return false;
+  for (int q = 0; q < a.npoints; ++q) {
+    const abft_point &p = a.points[q], &r = b.points[q];
+    if (p.di != r.di || p.dj != r.dj || p.dk != r.dk || p.w != r.w) return false;
+  }
+  for (int q = 0; q < a.nsources; ++q) {
+    const abft_source &s = a.sources[q], &r = b.sources[q];
+    if (s.coef != r.coef || s.scalar != r.scalar || (s.field == nullptr) != (r.field == nullptr)) return false;
+  }
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
 int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
   if (!hs || n < 2) return ABFT_EINVAL;
   for (int i = 0; i < n; ++i) {
     abft_stencil* h = hs[i];
     if (!h || h->grouped || h->comm || h->cfg.nranks != n || h->cfg.rank != i) return ABFT_EINVAL;
     const abft_config &a = h->cfg, &b = hs[0]->cfg;
-    if (a.nx != b.nx || a.ny != b.ny || a.nz_global != b.nz_global || a.dtype != b.dtype ||
-        a.mode != b.mode || a.delta != b.delta || a.npoints != b.npoints)
-      return ABFT_EINVAL;
+    if (!same_problem(a, b)) return ABFT_EINVAL;
     if (i + 1 < n && a.z_begin + a.z_count != hs[i + 1]->cfg.z_begin) return ABFT_EINVAL;
     if (h->sweeps != 0) return ABFT_EINVAL;
   }
   Group G(hs, hs + n);
+  DevScope ds(hs[0]);
   // fused halo when every neighbour's memory is directly addressable: same
   // device, or a peer GPU with peer access (NVLink); ABFT_GROUP_COPY=1 keeps
   // the device-copy exchange
@@ -1025,6 +1075,7 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
     h->grouped = true;
     h->fused = fused;
     h->members = G;
+    on_dev(h);   // events belong to the member's device (recorded on its stream)
     CK(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_pulled, cudaEventDisableTiming));
   }
@@ -1038,17 +1089,20 @@ int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps)
     if (!hs[i] || !hs[i]->grouped || hs[i]->members.size() != (size_t)n || hs[i]->members[i] != hs[i])
       return ABFT_EINVAL;
   Group G(hs, hs + n);
+  DevScope ds(hs[0]);
   return step_group(G, nsweeps);
 }
 
 int abft_stencil_step(abft_stencil* h, int32_t n) {
   if (!h || n < 0 || h->grouped) return ABFT_EINVAL;
+  DevScope ds(h);
   Group G{h};
   return step_group(G, n);
 }
 
 int abft_stencil_sweep(abft_stencil* h) {
   if (!h || h->grouped) return ABFT_EINVAL;
+  DevScope ds(h);
   if (h->cfg.mode == ABFT_MODE_OFFLINE) return ABFT_EINVAL;
   Group G{h};
   if (h->cfg.mode == ABFT_MODE_NONE) return none_sweep(G);
@@ -1071,6 +1125,7 @@ int abft_stencil_sweep(abft_stencil* h) {
 
 int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b) {
   if (!h || h->grouped || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  DevScope ds(h);
   TRY(clear_summaries(h));
   CK(cudaMemsetAsync(&h->st->flag_a, 0, 2 * sizeof(long long), h->stream));
   int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
@@ -1088,6 +1143,7 @@ int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b) {
 
 int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected) {
   if (!h || h->grouped || h->cfg.mode != ABFT_MODE_ONLINE || !h->pending_check) return ABFT_EINVAL;
+  DevScope ds(h);
   CK(cudaMemsetAsync(&h->st->ncorr, 0, sizeof(long long), h->stream));
   int r = launch_check(h, h->prev, h->cur, h->gA[h->gen_prev], h->gB[h->gen_prev], h->gA[h->gen],
                        h->gB[h->gen], nullptr, nullptr, nullptr, nullptr, CK_FROM_SUMMARY | CK_CORRECT,
@@ -1138,6 +1194,7 @@ int abft_stencil_set_faults(abft_stencil* h, const abft_fault* f, int32_t n) {
 
 int abft_stencil_field(abft_stencil* h, void** dev_ptr, int64_t* pitch) {
   if (!h || !dev_ptr) return ABFT_EINVAL;
+  DevScope ds(h);
   CK(cudaStreamSynchronize(h->stream));
   *dev_ptr = h->fb[h->cur] + (size_t)h->L.plane * h->L.esz;
   if (pitch) *pitch = h->L.px;
@@ -1146,6 +1203,7 @@ int abft_stencil_field(abft_stencil* h, void** dev_ptr, int64_t* pitch) {
 
 int abft_stencil_read_field(abft_stencil* h, void* dst) {
   if (!h || !dst) return ABFT_EINVAL;
+  DevScope ds(h);
   const size_t esz = h->L.esz;
   CK(cudaMemcpy2DAsync(dst, h->cfg.nx * esz, h->fb[h->cur] + (size_t)h->L.plane * esz, h->L.px * esz,
                        h->cfg.nx * esz, h->cfg.ny * h->cfg.z_count, cudaMemcpyDefault, h->stream));
@@ -1155,6 +1213,7 @@ int abft_stencil_read_field(abft_stencil* h, void* dst) {
 
 int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
   if (!h || !A || !B) return ABFT_EINVAL;
+  DevScope ds(h);
   const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
   int g = h->gen, ga = h->gen;
   if (h->cfg.mode == ABFT_MODE_NONE) {  // no running checksums: compute them now (Eqs. 2-3)
@@ -1181,6 +1240,7 @@ int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
 
 int abft_stencil_stats(abft_stencil* h, abft_stats* o) {
   if (!h || !o) return ABFT_EINVAL;
+  DevScope ds(h);
   long long c[9];
   CK(cudaMemcpyAsync(c, h->st->cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -1198,6 +1258,7 @@ int abft_stencil_stats(abft_stencil* h, abft_stats* o) {
 
 int abft_stencil_records(abft_stencil* h, abft_record* out, int32_t cap, int64_t* n) {
   if (!h || cap < 0 || (cap > 0 && !out)) return ABFT_EINVAL;
+  DevScope ds(h);
   unsigned long long nrec = 0;
   CK(cudaMemcpyAsync(&nrec, &h->st->nrec, sizeof(nrec), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -1212,6 +1273,7 @@ int abft_stencil_records(abft_stencil* h, abft_record* out, int32_t cap, int64_t
 
 int abft_stencil_status(abft_stencil* h) {
   if (!h) return ABFT_EINVAL;
+  DevScope ds(h);
   int w = 0;
   CK(cudaMemcpyAsync(&w, &h->st->worst, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -1230,6 +1292,7 @@ int abft_stencil_profile(abft_stencil* h, int32_t enable) {
 int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_n, double* k2_ms,
                               int64_t* k2_n, int32_t geo[6]) {
   if (!h) return ABFT_EINVAL;
+  DevScope ds(h);
   CK(cudaStreamSynchronize(h->stream));
   double t[3] = {0, 0, 0};
   int64_t n[3] = {0, 0, 0};
@@ -1253,6 +1316,7 @@ int abft_stencil_profile_read(abft_stencil* h, double* k1_ms, int64_t* k1_n, dou
 
 int abft_stencil_destroy(abft_stencil* h) {
   if (!h) return ABFT_EINVAL;
+  DevScope ds(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto e : h->ev) cudaEventDestroy(e);
   if (h->ev_ready) cudaEventDestroy(h->ev_ready);

@@ -15,6 +15,7 @@ constexpr int kMaxPoints = 27;   // radius-1 stencils in 3D
 constexpr int kMaxSources = 4;
 constexpr int kMaxFaultsPerLaunch = 64;   // scheduled flips per sweep and slab (set_faults checks)
 constexpr int kRecordCap = 4096;
+constexpr int kMaxDevices = 64;          // per-device launch attributes
 
 // ------------------------------------------------------------------ shapes
 // The sweep evaluates the points of S in the caller's order (the FMA chain is

@@ -485,3 +485,36 @@ def test_recompute_layer_explicit_api():
     assert sorted((r["sweep"], r["z"], r["y"], r["x"], r["status"]) for r in g["records"]) == \
         sorted((r["sweep"], r["z"], r["y"], r["x"], r["status"]) for r in o["records"])
     assert g["stats"]["corrected"] == len(faults)
+
+
+# ---- forms 0 / 1: several flips in one layer (P:663-667 pairing, Q13 / Q14) --
+
+@pytest.mark.parametrize("form", [0, 1])
+@pytest.mark.parametrize("checksums", [0, 1])
+def test_multi_flip_layer_uncorrectable_and_unlocated(form, checksums):
+    # per layer and sweep: two flips in different rows and columns (a and b
+    # flag twice: UNCORRECTABLE), two in one row (a twice, b once:
+    # UNCORRECTABLE), and on a 1024 x 8 layer a flip above eps|a| but below
+    # eps|b| (only a flags: UNLOCATED under BOTH).  Under LAZY the layer is
+    # examined only when b flags, so the first two still report.
+    p = make_problem("cfg2", nx=96, ny=80, nz=6, sweeps=8, correction_form=form, checksums=checksums)
+    faults = [Fault(3, 1, 10, 20, 29), Fault(3, 1, 50, 70, 28),          # a: 2, b: 2
+              Fault(5, 4, 33, 5, 29), Fault(5, 4, 33, 90, 30),           # a: 2, b: 1
+              Fault(6, 2, 7, 7, 29)]                                     # single: corrected
+    g, o = parity(p, faults=faults)
+    st = sorted((r["sweep"], r["z"], r["status"]) for r in o["records"])
+    assert (3, 1, abft.REC_UNCORRECTABLE) in st and (5, 4, abft.REC_UNCORRECTABLE) in st
+    assert (6, 2, abft.REC_CORRECTED) in st
+    assert g["status"] == abft.ABFT_DETECTED_UNCORRECTABLE
+    # only one vector flags: rows of 1024 cells, columns of 8 (~333 each):
+    # bit 12 of a value ~333 (delta 0.125) exceeds eps|a| ~ 0.027 but not eps|b| ~ 3.4
+    q = make_problem("cfg2", nx=1024, ny=8, nz=3, sweeps=4, correction_form=form, checksums=checksums)
+    g, o = parity(q, faults=[Fault(2, 1, 3, 500, 12)])
+    if checksums == 0:
+        assert [r["status"] for r in o["records"]] == [abft.REC_UNLOCATED]
+    else:
+        assert o["records"] == []       # b never flagged: the lazy check does not look at a
+    # b-only under LAZY: columns of 1024 cells, rows of 8
+    q = make_problem("cfg2", nx=8, ny=1024, nz=3, sweeps=4, correction_form=form, checksums=checksums)
+    g, o = parity(q, faults=[Fault(2, 1, 500, 3, 12)])
+    assert [r["status"] for r in o["records"]] == [abft.REC_UNLOCATED]

@@ -209,6 +209,35 @@ def test_sweep_sources_hotspot_closed_form():
     assert (out == 256.0 + 0.5 * 2.0 + 0.25 * 8.0).all()
 
 
+def test_constant_sums_fp32_use_dtype_rounded_operands():
+    # c_x, c_y of Theorem 1 ("pre-computed" P:392) for an fp32 problem:
+    # the constant C_{x,y} of Eq. 1 as the sweep applies it, i.e. with the
+    # coefficients and the scalar rounded to the field dtype (Q23).  Exact
+    # rational brute force: every product of two fp32 values is exact in
+    # fp64, so the oracle's fp64 sums may differ from the exact sum only by
+    # their own rounding (<= ny ulps); an oracle that used the unrounded
+    # fp64 coefficients (0.001, 0.05) would be off by ~1e-8 relative.
+    nz, ny, nx = 3, 6, 8
+    p = Problem("t", nx, ny, nz, "f32", [(0, 0, 0, 1.0)],
+                [(0.001, True, 0.0), (0.05, False, 80.0)])
+    P = np.random.default_rng(5).random((nz, ny, nx)).astype(np.float32)
+    cA, cB = O.constant_sums(O.OProblem(p, [P]))
+    f = lambda v: Fraction(float(np.float32(v)))
+    C = [[[f(0.001) * Fraction(float(P[z, y, x])) + f(0.05) * f(80.0) for x in range(nx)]
+          for y in range(ny)] for z in range(nz)]
+    for z in range(nz):
+        for x in range(nx):
+            ex = sum(C[z][y][x] for y in range(ny))
+            assert abs(Fraction(cA[z, x]) - ex) <= ex * Fraction(1, 2 ** 49)
+        for y in range(ny):
+            ex = sum(C[z][y][x] for x in range(nx))
+            assert abs(Fraction(cB[z, y]) - ex) <= ex * Fraction(1, 2 ** 49)
+    # the unrounded coefficients are measurably different (the pin can fail)
+    raw = sum(Fraction(0.001) * Fraction(float(P[0, y, 0])) + Fraction(0.05) * Fraction(80.0)
+              for y in range(ny))
+    assert abs(Fraction(cA[0, 0]) - raw) > raw * Fraction(1, 10 ** 9)
+
+
 # ------------------------------------------------------ Theorem 1 (prediction)
 
 def _fsum_checksums(u):
