@@ -123,6 +123,7 @@ class Problem:
     sweeps: int = 1
     correction_form: int = 0            # 0 re-summed Eq. 8, 1 literal Eq. 8
     checksums: int = 0                  # 0 a and b every sweep, 1 b every sweep + a on detection
+    recovery: int = 0                   # offline: 0 full rollback, 1 re-execute the flagged layers' light cone
     init: Tuple[float, float] = (0.0, 1.0)
     power: Optional[Tuple[float, float]] = None
     fault_recipe: str = "none"

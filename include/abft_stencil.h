@@ -80,6 +80,16 @@ typedef enum { ABFT_MODE_NONE = 0, ABFT_MODE_ONLINE = 1, ABFT_MODE_OFFLINE = 2 }
  * OFFLINE windows and the explicit sweep()/check()/correct() API always use
  * BOTH. */
 typedef enum { ABFT_CK_BOTH = 0, ABFT_CK_LAZY = 1 } abft_checksum_policy;
+/* What a dirty OFFLINE window re-executes.  ROLLBACK: the whole window from
+ * its checkpoint.  PARTIAL: stencil locality (P:107-108,
+ * P:743-745 "exploit stencil locality to reduce the re-execution cost"): an
+ * error injected in a window of L sweeps spreads at most L - 1 layers, so
+ * only the layers within 2 (L - 1) of a flagged layer (over all ranks) are
+ * re-executed from the checkpoint -- the light cone of that range, sweep by
+ * sweep -- and re-checked; every other layer keeps its first execution
+ * (Q28).  Equal to ROLLBACK whenever every error of the window is
+ * detected; an undetected one outside the range is not erased. */
+typedef enum { ABFT_RECOVER_ROLLBACK = 0, ABFT_RECOVER_PARTIAL = 1 } abft_recovery;
 /* abft_record.status */
 typedef enum {
   ABFT_REC_CORRECTED = 1,     /* located by intersection, corrected (Eq. 8)      */
@@ -144,6 +154,8 @@ typedef struct {
                                  all ranks (one process per GPU, nranks > 1); NULL
                                  for nranks == 1 or for a local group member (see
                                  abft_stencil_group) */
+  int32_t recovery;     /* abft_recovery: what an OFFLINE dirty window re-executes */
+  int32_t pad;
 } abft_config;
 
 /* A scheduled single bit-flip (fault model P:783-785): at sweep `sweep`

@@ -471,11 +471,15 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
        sweeps; on mismatch the window is recomputed from the checkpoint taken
        at its start. */
     void* ckpt = malloc(fb);
+    void* first = p->recovery == 1 ? malloc(fb) : NULL;
     int64_t s = sweep0;
     const int64_t end = sweep0 + nsweeps;
     while (s < end) {
       const int64_t wend = (s + p->delta < end) ? s + p->delta : end;
       memcpy(ckpt, cur, fb);                         /* in-memory checkpoint */
+      /* layers the window check covers: all, and after a partial
+         re-execution only the re-executed ones (Q28) */
+      int64_t zlo = 0, zhi = nz - 1;
       for (int32_t attempt = 0; attempt < 2; attempt++) {
         memcpy(PA, Ap, sizeof(double) * nz * nx);    /* interpolation starts from */
         memcpy(PB, Bp, sizeof(double) * nz * ny);    /* the checkpoint's checksums */
@@ -488,10 +492,18 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
           void* tv = cur; cur = nxt; nxt = tv;
           stats->sweeps++;
         }
+        if (attempt == 1 && p->recovery == 1) {
+          /* partial re-execution (Q28): only layers zlo..zhi come from the
+             re-execution; every other layer keeps the first execution's
+             values (no detected error reached it) */
+          const size_t lb = (size_t)nx * ny * esz(p->dtype);
+          for (int64_t z = 0; z < nz; z++)
+            if (z < zlo || z > zhi) memcpy((char*)cur + z * lb, (const char*)first + z * lb, lb);
+        }
         or_checksums(p, cur, An, Bn);
         stats->windows++;
-        int64_t dirty = 0;
-        for (int64_t z = 0; z < nz; z++) {
+        int64_t dirty = 0, zmin = nz, zmax = -1;
+        for (int64_t z = zlo; z <= zhi; z++) {
           int64_t na = 0, nb = 0, x0 = -1, y0 = -1;
           for (int64_t x = 0; x < nx; x++)
             if (or_flag(PA[z * nx + x], An[z * nx + x], p->eps)) { if (x0 < 0) x0 = x; na++; }
@@ -499,6 +511,8 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
             if (or_flag(PB[z * ny + y], Bn[z * ny + y], p->eps)) { if (y0 < 0) y0 = y; nb++; }
           if (na + nb == 0) continue;
           dirty++;
+          if (z < zmin) zmin = z;
+          if (z > zmax) zmax = z;
           stats->detections++;
           or_record r;
           memset(&r, 0, sizeof r);
@@ -510,6 +524,17 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
         if (!dirty) break;
         if (attempt == 0) {
           stats->rollbacks++;                        /* rollback to t - delta */
+          if (p->recovery == 1) {
+            /* stencil locality, reading Q28: an error
+               injected in this window of L sweeps has spread at most L - 1
+               layers from its origin, and every flagged layer lies within
+               that reach, so everything it touched is within 2 (L - 1)
+               layers of a flagged one */
+            const int64_t r = 2 * (wend - s - 1);
+            zlo = zmin - r < 0 ? 0 : zmin - r;
+            zhi = zmax + r > nz - 1 ? nz - 1 : zmax + r;
+            memcpy(first, cur, fb);
+          }
           if (cur != ckpt) memcpy(cur, ckpt, fb);
         } else {
           stats->persistent++;
@@ -522,6 +547,7 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
       s = wend;
     }
     free(ckpt);
+    free(first);
   }
   if (cur != u) memcpy(u, cur, fb);
   free(tmp);

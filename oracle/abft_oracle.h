@@ -64,6 +64,11 @@ typedef struct {
   int32_t checksums;   /* online: 0 = a and b every sweep (SURVEY Q8 reading);
                           1 = b every sweep, a only for layers whose b flags
                           (the paper's recommendation) */
+  int32_t recovery;    /* offline, dirty window: 0 = roll back to the window's
+                          checkpoint and re-execute it;
+                          1 = re-execute only the layers an error detected in
+                          the window can have reached (stencil locality,
+                          P:107-108; Q28) */
 } or_problem;
 
 /* flip bit `bit` of cell idx */

@@ -54,7 +54,8 @@ class ProblemS(C.Structure):
                 ("npoints", C.c_int32), ("nsources", C.c_int32),
                 ("points", C.POINTER(Point)), ("sources", C.POINTER(Source)),
                 ("eps", C.c_double), ("mode", C.c_int32), ("delta", C.c_int32),
-                ("correction_form", C.c_int32), ("checksums", C.c_int32)]
+                ("correction_form", C.c_int32), ("checksums", C.c_int32),
+                ("recovery", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -128,6 +129,7 @@ class OProblem:
         s.eps, s.mode, s.delta = prob.eps, prob.mode, prob.delta
         s.correction_form = prob.correction_form
         s.checksums = getattr(prob, "checksums", 0)
+        s.recovery = getattr(prob, "recovery", 0)
         self.s = s
 
     @property

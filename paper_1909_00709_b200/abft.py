@@ -22,6 +22,7 @@ ABFT_F32, ABFT_F64 = 0, 1
 ABFT_BC_CLAMP, ABFT_BC_PERIODIC, ABFT_BC_ZERO, ABFT_BC_CONSTANT = 0, 1, 2, 3
 ABFT_MODE_NONE, ABFT_MODE_ONLINE, ABFT_MODE_OFFLINE = 0, 1, 2
 ABFT_CK_BOTH, ABFT_CK_LAZY = 0, 1
+ABFT_RECOVER_ROLLBACK, ABFT_RECOVER_PARTIAL = 0, 1
 REC_CORRECTED, REC_UNLOCATED, REC_UNCORRECTABLE, REC_WINDOW_DIRTY, REC_PERSISTENT, REC_RECOMPUTED, REC_VERIFIED = 1, 2, 3, 4, 5, 6, 7
 
 EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_step",
@@ -51,7 +52,8 @@ class abft_config(C.Structure):
                 ("points", C.POINTER(abft_point)), ("sources", C.POINTER(abft_source)),
                 ("epsilon", C.c_double), ("mode", C.c_int32), ("delta", C.c_int32),
                 ("correction_form", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("checksum_policy", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+                ("checksum_policy", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("recovery", C.c_int32), ("pad", C.c_int32)]
 
 
 class abft_fault(C.Structure):
@@ -147,7 +149,7 @@ def make_config(nx: int, ny: int, nz: int, dtype, points: Sequence[Tuple[int, in
                 mode: int = ABFT_MODE_ONLINE, delta: int = 1, correction_form: int = 0,
                 z_begin: int = 0, z_count: Optional[int] = None, rank: int = 0,
                 nranks: int = 1, nccl_unique_id: Optional[bytes] = None,
-                checksum_policy: int = 0):
+                checksum_policy: int = 0, recovery: int = 0):
     """abft_config for the problem as the paper states it (Eq. 1: stencil points
     (di, dj, dk, w) in evaluation order + constant-term sources
     (coef, device field or None, scalar); BC; threshold; offline period).
@@ -173,6 +175,7 @@ def make_config(nx: int, ny: int, nz: int, dtype, points: Sequence[Tuple[int, in
     c.epsilon, c.mode, c.delta, c.correction_form = epsilon, mode, delta, correction_form
     c.rank, c.nranks = rank, nranks
     c.checksum_policy = checksum_policy
+    c.recovery = recovery
     idbuf = None
     if nccl_unique_id is not None:
         idbuf = C.create_string_buffer(bytes(nccl_unique_id), 128)
@@ -364,7 +367,8 @@ def problem_config(p, power: Optional[torch.Tensor] = None, **kw):
             raise ValueError("problem has a field source: pass `power`")
         srcs.append((coef, power if has_field else None, scalar))
     args = dict(bc=p.bc, bc_value=p.bc_value, epsilon=p.eps, mode=p.mode, delta=p.delta,
-                correction_form=p.correction_form, checksum_policy=getattr(p, "checksums", 0))
+                correction_form=p.correction_form, checksum_policy=getattr(p, "checksums", 0),
+                recovery=getattr(p, "recovery", 0))
     args.update(kw)
     return make_config(p.nx, p.ny, p.nz, p.dtype, p.points, srcs, **args)
 

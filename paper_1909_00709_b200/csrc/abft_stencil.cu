@@ -145,6 +145,7 @@ int validate(const abft_config* c) {
   if (c->mode == ABFT_MODE_OFFLINE && c->delta < 1) return ABFT_EINVAL;
   if (c->correction_form < 0 || c->correction_form > 2) return ABFT_EINVAL;
   if (c->checksum_policy != ABFT_CK_BOTH && c->checksum_policy != ABFT_CK_LAZY) return ABFT_EINVAL;
+  if (c->recovery != ABFT_RECOVER_ROLLBACK && c->recovery != ABFT_RECOVER_PARTIAL) return ABFT_EINVAL;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
   if (c->nranks > 1) {
     if ((c->rank == 0) != (c->z_begin == 0)) return ABFT_EINVAL;
@@ -366,8 +367,16 @@ CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, c
 }
 
 // K1: step (1)
-int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, int64_t sweep) {
+// za / zb: the slab-local layers [za, zb) to compute (partial re-execution;
+// zb < 0: the whole slab)
+int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, int64_t sweep,
+              int za = 0, int zb = -1) {
   SweepParams p = h->sp;
+  if (zb < 0) zb = (int)h->cfg.z_count;
+  p.zr0 = za;
+  p.zr1 = zb;
+  dim3 grid = h->grid1;
+  grid.z = (unsigned)((zb - za + h->zchunk - 1) / h->zchunk);
   p.out = h->fb[dst];
   p.uin = h->fb[src];
   p.peerU[0] = p.peerU[1] = nullptr;
@@ -401,8 +410,8 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
   h->executed++;
   cudaEvent_t* pe = prof_begin(h, 1);
   const cudaError_t e = h->cfg.dtype == ABFT_F32
-            ? launch_k1_f32(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p)
-            : launch_k1_f64(h->shape, chk, var, h->grid1, h->stream, h->tm_u[src], p);
+            ? launch_k1_f32(h->shape, chk, var, grid, h->stream, h->tm_u[src], p)
+            : launch_k1_f64(h->shape, chk, var, grid, h->stream, h->tm_u[src], p);
   prof_end(h, pe);
   h->launches++;
   CK(e);
@@ -413,7 +422,7 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
 int launch_check(abft_stencil* h, const CheckParams& p) {
   on_dev(h);
   cudaEvent_t* pe = prof_begin(h, 2);
-  cudaError_t e = launch_k2(h->cfg.dtype, h->shape, (int)h->cfg.z_count, h->stream, p);
+  cudaError_t e = launch_k2(h->cfg.dtype, h->shape, h->stream, p);
   prof_end(h, pe);
   h->launches++;
   CK(e);
@@ -576,11 +585,13 @@ int halo_exchange(Group& G, const XSpec& x) {
 // the interior rows of a checksum generation, which K1 accumulates into; the
 // halo rows belong to the neighbours' exchange (a fused neighbour may already
 // have written them on its own stream)
-int zero_gen(abft_stencil* h, int g) {
+int zero_gen(abft_stencil* h, int g, int za = 0, int zb = -1) {
   on_dev(h);
-  const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
-  CK(cudaMemsetAsync(h->gA[g] + nx, 0, sizeof(double) * zc * nx, h->stream));
-  CK(cudaMemsetAsync(h->gB[g] + ny, 0, sizeof(double) * zc * ny, h->stream));
+  const int64_t nx = h->cfg.nx, ny = h->cfg.ny;
+  if (zb < 0) zb = (int)h->cfg.z_count;
+  if (zb <= za) return ABFT_OK;
+  CK(cudaMemsetAsync(h->gA[g] + (za + 1) * nx, 0, sizeof(double) * (zb - za) * nx, h->stream));
+  CK(cudaMemsetAsync(h->gB[g] + (za + 1) * ny, 0, sizeof(double) * (zb - za) * ny, h->stream));
   return ABFT_OK;
 }
 
@@ -644,22 +655,80 @@ int none_sweep(Group& G) {
   return ABFT_OK;
 }
 
-// flagged layers of the last window check, summed over every slab of the job
-int read_dirty(Group& G, int* dirty) {
+// the last window check over every slab of the job: flagged layers (> 0:
+// dirty) and the global extent [zmin, zmax] of the flagged layers
+int read_dirty(Group& G, int* dirty, int64_t* zmin, int64_t* zmax) {
   *dirty = 0;
+  int ext[2] = {0, 0};
   for (abft_stencil* h : G) {
     on_dev(h);
     if (G.size() == 1 && h->cfg.nranks > 1) {
+      // dirty, zext[0], zext[1] are adjacent ints: one max-reduction (a
+      // count's maximum is nonzero iff any rank's is)
       NcclApi* n = nccl_api();
       if (!n) return ABFT_ENCCL;
-      if (n->allReduce(&h->st->dirty, &h->st->dirty, 1, ncclInt32, ncclSum, h->comm, h->stream) !=
+      if (n->allReduce(&h->st->dirty, &h->st->dirty, 3, ncclInt32, ncclMax, h->comm, h->stream) !=
           ncclSuccess)
         return ABFT_ENCCL;
     }
-    int d = 0;
-    CK(cudaMemcpyAsync(&d, &h->st->dirty, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    int d[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(d, &h->st->dirty, sizeof(d), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    *dirty += d;
+    *dirty += d[0];
+    ext[0] = std::max(ext[0], d[1]);
+    ext[1] = std::max(ext[1], d[2]);
+  }
+  *zmin = 0x7fffffffLL - ext[0];
+  *zmax = (int64_t)ext[1] - 1;
+  return ABFT_OK;
+}
+
+// Partial re-execution of a dirty window of L sweeps (recovery PARTIAL,
+// P:107-108, Q28): only the global layers [zlo, zhi]
+// are recomputed from the checkpoint.  Sweep k re-executes the light cone
+// [zlo - (L - k), zhi + (L - k)] of that range, reading sweep k - 1's cone;
+// the cone of sweep k < L goes to the two buffers other than `last` (the
+// first execution's result), ping-pong -- the checkpoint is read by sweep 1
+// only -- and sweep L writes [zlo, zhi] into `last`, whose other layers keep
+// the first execution.  The predictions P are re-advanced over the same
+// cones, the actual checksums of [zlo, zhi] recomputed and compared.
+int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, int ckgen, int gend,
+                   int64_t s0) {
+  int other = 0;
+  while (other == ck || other == last) ++other;
+  int src = ck;
+  for (int k = 1; k <= L; ++k) {
+    const int64_t s = s0 + k;
+    const bool end = k == L;
+    const int dst = end ? last : (src == ck ? other : ck);
+    const int64_t glo = std::max<int64_t>(0, zlo - (L - k));
+    const int64_t ghi = std::min<int64_t>(G[0]->cfg.nz_global - 1, zhi + (L - k));
+    set_fwd(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, k & 1});
+    for (abft_stencil* h : G) {
+      const int64_t zb0 = h->cfg.z_begin;
+      const int za = (int)std::max<int64_t>(0, glo - zb0);
+      const int zb = (int)std::min<int64_t>(h->cfg.z_count, ghi - zb0 + 1);
+      if (za >= zb) { h->executed++; continue; }   // the cone misses this slab
+      const double* pA = k == 1 ? h->gA[ckgen] : h->PA[(k - 1) & 1];
+      const double* pB = k == 1 ? h->gB[ckgen] : h->PB[(k - 1) & 1];
+      CheckParams c;
+      if (!end) {
+        TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s, za, zb));
+        c = make_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[k & 1], h->PB[k & 1], nullptr,
+                       nullptr, CK_STORE_PRED, s);
+      } else {
+        TRY(zero_gen(h, gend, za, zb));
+        TRY(launch_k1(h, src, dst, h->gA[gend], h->gB[gend], K1_CK_AB, s, za, zb));
+        c = make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
+                       nullptr, CK_COMPARE | CK_OFFLINE_END | CK_PERSIST, s);
+      }
+      c.zr0 = za;
+      c.zr1 = zb;
+      TRY(launch_check(h, c));
+    }
+    TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, k & 1}));
+    for (abft_stencil* h : G) h->sweeps = s;
+    src = dst;
   }
   return ABFT_OK;
 }
@@ -668,51 +737,65 @@ int read_dirty(Group& G, int* dirty) {
 // the checkpoint (current buffer + its actual checksums), the prediction
 // vectors advanced once per sweep (Q17), compared at the window end; on
 // mismatch -- anywhere in the job -- every slab recomputes the window from
-// its checkpoint (rotation of three field buffers: no copy); a second
-// mismatch is a persistent error.
+// its checkpoint (rotation of three field buffers: no copy), or only the
+// light cone of the flagged layers (recovery PARTIAL); a second mismatch is a
+// persistent error.
 int offline_window(Group& G, int L) {
   abft_stencil* h0 = G[0];
   const int ck = h0->cur, ckgen = h0->gen, gend = (h0->gen + 1) % 3;
   const int64_t s0 = h0->sweeps;
+  const bool partial = h0->cfg.recovery == ABFT_RECOVER_PARTIAL;
   int others[2], k = 0;
   for (int b = 0; b < 3; ++b)
     if (b != ck) others[k++] = b;
   int last = ck;
   int worst = ABFT_OK;
+  int64_t zlo = 0, zhi = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    for (abft_stencil* h : G) { on_dev(h); CK(cudaMemsetAsync(&h->st->dirty, 0, sizeof(int), h->stream)); }
-    int src = ck;
-    for (int t = 1; t <= L; ++t) {
-      const int64_t s = s0 + t;
-      const int dst = (src == others[0]) ? others[1] : others[0];
-      const bool end = (t == L);
-      set_fwd(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1});
-      // P^{t-1}: the checkpoint's actual checksums for t = 1, else slot (t-1)&1
-      for (abft_stencil* h : G) {
-        const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
-        const double* pB = t == 1 ? h->gB[ckgen] : h->PB[(t - 1) & 1];
-        if (!end) {
-          TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
-          TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
-                           nullptr, nullptr, CK_STORE_PRED, s));
-        } else {
-          TRY(zero_gen(h, gend));
-          TRY(sweep_checked(h, src, dst, h->gA[gend], h->gB[gend],
-                            make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr,
-                                       nullptr, nullptr, nullptr,
-                                       CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s),
-                            s));
+    for (abft_stencil* h : G) { on_dev(h); CK(cudaMemsetAsync(&h->st->dirty, 0, 3 * sizeof(int), h->stream)); }
+    if (attempt == 1 && partial) {
+      TRY(partial_window(G, L, zlo, zhi, ck, last, ckgen, gend, s0));
+    } else {
+      int src = ck;
+      for (int t = 1; t <= L; ++t) {
+        const int64_t s = s0 + t;
+        const int dst = (src == others[0]) ? others[1] : others[0];
+        const bool end = (t == L);
+        set_fwd(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1});
+        // P^{t-1}: the checkpoint's actual checksums for t = 1, else slot (t-1)&1
+        for (abft_stencil* h : G) {
+          const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
+          const double* pB = t == 1 ? h->gB[ckgen] : h->PB[(t - 1) & 1];
+          if (!end) {
+            TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
+            TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
+                             nullptr, nullptr, CK_STORE_PRED, s));
+          } else {
+            TRY(zero_gen(h, gend));
+            TRY(sweep_checked(h, src, dst, h->gA[gend], h->gB[gend],
+                              make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr,
+                                         nullptr, nullptr, nullptr,
+                                         CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s),
+                              s));
+          }
         }
+        TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1}));
+        for (abft_stencil* h : G) h->sweeps = s;
+        src = dst;
       }
-      TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1}));
-      for (abft_stencil* h : G) h->sweeps = s;
-      src = dst;
+      last = src;
     }
-    last = src;
     int dirty = 0;
-    TRY(read_dirty(G, &dirty));
+    int64_t zmin = 0, zmax = 0;
+    TRY(read_dirty(G, &dirty, &zmin, &zmax));
     for (abft_stencil* h : G) h->windows++;
     if (!dirty) break;
+    if (attempt == 0) {
+      // re-execution range of a partial recovery: every layer an error of
+      // this window that was flagged can have reached (Q28)
+      zlo = std::max<int64_t>(0, zmin - 2 * (L - 1));
+      zhi = std::min<int64_t>(h0->cfg.nz_global - 1, zmax + 2 * (L - 1));
+    }
     for (abft_stencil* h : G) {
       if (attempt == 0) {
         h->rollbacks++;  // rollback to the checkpoint, recompute
@@ -917,6 +1000,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   SweepParams& sp = h->sp;
   memset(&sp, 0, sizeof(sp));
   sp.nx = (int)nx; sp.ny = (int)ny; sp.zc = (int)zc; sp.zchunk = h->zchunk;
+  sp.zr0 = 0; sp.zr1 = (int)zc;
   sp.bc = cfg->bc;
   sp.g = cfg->bc == ABFT_BC_CONSTANT ? rnd(cfg->dtype, cfg->bc_value) : 0.0;
   sp.src = h->src_field;
@@ -956,6 +1040,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   cp.eps = cfg->epsilon;
   cp.form = cfg->correction_form;
   cp.z_begin = cfg->z_begin;
+  cp.zr0 = 0; cp.zr1 = (int)zc;
 
   // constant ghosts: the halo layers no neighbour owns are the
   // ghost layers of z (zmap); zero ghosts are the init memset
@@ -1018,7 +1103,7 @@ bool same_problem(const abft_config& a, const abft_config& b) {
   if (a.nx != b.nx || a.ny != b.ny || a.nz_global != b.nz_global || a.dtype != b.dtype ||
       a.mode != b.mode || a.delta != b.delta || a.npoints != b.npoints || a.nsources != b.nsources ||
       a.bc != b.bc || a.epsilon != b.epsilon || a.correction_form != b.correction_form ||
-      a.checksum_policy != b.checksum_policy)
+      a.checksum_policy != b.checksum_policy || a.recovery != b.recovery)
     return false;
   if (a.bc == ABFT_BC_CONSTANT && a.bc_value != b.bc_value) return false;
   for (int q = 0; q < a.npoints; ++q) {

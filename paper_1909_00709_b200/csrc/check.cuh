@@ -246,6 +246,9 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
       push_record(p.st, r);
       bump(p.st, ST_DETECT);
       atomicAdd(&p.st->dirty, 1);
+      // the flagged layers' extent (partial re-execution, Q28)
+      atomicMax(&p.st->zext[0], (int)(0x7fffffffLL - r.z));
+      atomicMax(&p.st->zext[1], (int)(r.z + 1));
     }
     return;
   }
@@ -369,7 +372,7 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
 }
 template <typename T, int S, bool BCG>
 __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
-  const int z = blockIdx.x, bz = z + 1;
+  const int z = p.zr0 + blockIdx.x, bz = z + 1;
   const int tid = threadIdx.x, part = blockIdx.y, nparts = gridDim.y;
   LayerSummary* L = &p.summ[z];
   __shared__ int s_na, s_nb, s_xk, s_yk, s_last;
@@ -545,70 +548,113 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
 // ---------------------------------------------------------------- K0
 // Initial checksums a^0, b^0 of the trusted input (Eqs. 2-3) and c_x, c_y of
 // the constant term (Theorem 1, "pre-computed" P:392).  Each sum is
-// taken sequentially in ascending index order by one thread (coalesced
-// through a shared-memory transpose for the row sums), i.e. the same order as
-// the definition, so fp64-data results are reproducible.
+// taken sequentially in ascending index order by one thread -- the
+// definition's order, so sums of fp64 terms (c_x, c_y; fp64 data) are
+// reproducible bitwise -- with many loads in flight ahead of the dependent
+// additions: 8 rows per column thread (k0_colsum), one 128-byte segment of
+// its row per row thread (k0_rowsum, 16-byte vector loads).
 struct FieldVal {   // u of field buffer layer z (layer pitch `plane`, halo offset 1)
   const void* u;
   int64_t px, plane;
   int dtype;
-  __device__ __forceinline__ double operator()(int z, int y, int x) const {
-    const size_t i = (size_t)(z + 1) * plane + (size_t)y * px + x;
-    return dtype == ABFT_F32 ? (double)reinterpret_cast<const float*>(u)[i]
-                             : reinterpret_cast<const double*>(u)[i];
+  __device__ __forceinline__ const char* row(int z, int y) const {
+    return static_cast<const char*>(u) + ((size_t)(z + 1) * plane + (size_t)y * px) * (dtype == ABFT_F32 ? 4 : 8);
   }
+  __device__ __forceinline__ double val(double v, int) const { return v; }
 };
 struct ConstVal {   // C_{x,y} = sum_q coef_q * src_q (fp64, dtype-rounded operands)
   const void* field;
   int64_t fpx, fplane;
   int dtype, nsources, field_src;
   double coef[kMaxSources], scalar[kMaxSources];
-  __device__ __forceinline__ double operator()(int z, int y, int x) const {
+  __device__ __forceinline__ const char* row(int z, int y) const {
+    return field ? static_cast<const char*>(field) + ((size_t)z * fplane + (size_t)y * fpx) * (dtype == ABFT_F32 ? 4 : 8)
+                 : nullptr;
+  }
+  // C from the field value at this cell (unused without a field source)
+  __device__ __forceinline__ double val(double fv, int) const {
     double s = 0.0;
     for (int q = 0; q < nsources; ++q) {
-      double sv;
-      if (q == field_src) {
-        const size_t i = (size_t)z * fplane + (size_t)y * fpx + x;
-        sv = dtype == ABFT_F32 ? (double)reinterpret_cast<const float*>(field)[i]
-                               : reinterpret_cast<const double*>(field)[i];
-      } else {
-        sv = scalar[q];
-      }
-      const double t = __dmul_rn(coef[q], sv);
+      const double t = __dmul_rn(coef[q], q == field_src ? fv : scalar[q]);
       s = (q == 0) ? t : __dadd_rn(s, t);
     }
     return s;
   }
 };
+// element x of a row as fp64 (null row: a field-less constant term)
+__device__ __forceinline__ double k0_ld(const char* row, int dtype, int x) {
+  if (!row) return 0.0;
+  return dtype == ABFT_F32 ? (double)__ldg(reinterpret_cast<const float*>(row) + x)
+                           : __ldg(reinterpret_cast<const double*>(row) + x);
+}
 
-// A[z][x] = sum_y f(z, y, x); grid (zc, ceil(nx / 256)); out row stride nx, layer offset `off`
+// A[z][x] = sum_y f(z, y, x); 1D grid of zc x ceil(nx / 256) CTAs; out row
+// stride nx, layer offset `off`
 template <typename F>
-__global__ void __launch_bounds__(256) k0_colsum(F f, int nx, int ny, double* A, int off) {
-  const int z = blockIdx.x, x = blockIdx.y * 256 + threadIdx.x;
+__global__ void __launch_bounds__(256) k0_colsum(F f, int dtype, int nx, int ny, double* A, int off) {
+  const int64_t nxb = (nx + 255) / 256;
+  const int z = (int)(blockIdx.x / nxb), x = (int)(blockIdx.x % nxb) * 256 + threadIdx.x;
   if (x >= nx) return;
   double s = 0.0;
-  for (int y = 0; y < ny; ++y) s = __dadd_rn(s, f(z, y, x));
+  int y = 0;
+  for (; y + 8 <= ny; y += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = k0_ld(f.row(z, y + j), dtype, x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __dadd_rn(s, f.val(v[j], x));
+  }
+  for (; y < ny; ++y) s = __dadd_rn(s, f.val(k0_ld(f.row(z, y), dtype, x), x));
   A[(size_t)(z + off) * nx + x] = s;
 }
-// B[z][y] = sum_x f(z, y, x); grid (zc, ceil(ny / 128)), 128 threads, one row per thread
+
+// B[z][y] = sum_x f(z, y, x); one thread per row, 128-byte segments of the
+// row per step (rows are 16-byte aligned: padded pitch / TMA-legal source)
 template <typename F>
-__global__ void __launch_bounds__(128) k0_rowsum(F f, int nx, int ny, double* B, int off) {
-  __shared__ double tile[128][33];
-  const int z = blockIdx.x, yb = blockIdx.y * 128;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__global__ void __launch_bounds__(256) k0_rowsum(F f, int dtype, int nx, int ny, int zc, double* B, int off) {
+  const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (r >= (int64_t)zc * ny) return;
+  const int z = (int)(r / ny), y = (int)(r % ny);
+  const char* row = f.row(z, y);
   double s = 0.0;
-  for (int xc = 0; xc < nx; xc += 32) {
-    for (int rr = warp; rr < 128; rr += 4) {
-      const int y = yb + rr, x = xc + lane;
-      tile[rr][lane] = (y < ny && x < nx) ? f(z, y, x) : 0.0;
+  int x = 0;
+  if (dtype == ABFT_F32) {
+    for (; x + 32 <= nx; x += 32) {
+      float4 v[8];
+      if (row) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(row) + x / 4 + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s = __dadd_rn(s, f.val((double)v[j].x, x + 4 * j));
+        s = __dadd_rn(s, f.val((double)v[j].y, x + 4 * j + 1));
+        s = __dadd_rn(s, f.val((double)v[j].z, x + 4 * j + 2));
+        s = __dadd_rn(s, f.val((double)v[j].w, x + 4 * j + 3));
+      }
     }
-    __syncthreads();
-    const int m = min(32, nx - xc);
-    for (int c = 0; c < m; ++c) s = __dadd_rn(s, tile[threadIdx.x][c]);
-    __syncthreads();
+  } else {
+    for (; x + 16 <= nx; x += 16) {
+      double2 v[8];
+      if (row) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(reinterpret_cast<const double2*>(row) + x / 2 + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s = __dadd_rn(s, f.val(v[j].x, x + 2 * j));
+        s = __dadd_rn(s, f.val(v[j].y, x + 2 * j + 1));
+      }
+    }
   }
-  const int y = yb + threadIdx.x;
-  if (y < ny) B[(size_t)(z + off) * ny + y] = s;
+  for (; x < nx; ++x) s = __dadd_rn(s, f.val(k0_ld(row, dtype, x), x));
+  B[(size_t)(z + off) * ny + y] = s;
 }
 
 }  // namespace abft

@@ -90,6 +90,7 @@ struct DevState {
   long long cnt[9];        // mirrors abft_stats order
   int worst;               // 0 / 1 / 3
   int dirty;               // offline: flagged layers in the last window check
+  int zext[2];             // offline: INT_MAX - lowest and 1 + highest flagged global layer (0: none)
   long long flag_a, flag_b;  // explicit check(): flagged entries
   long long ncorr;           // explicit correct(): corrections
   int lazy_n[2];             // lazy checksum policy: layers whose b flagged, by sweep parity
@@ -160,10 +161,12 @@ struct CheckParams {
   double eps;
   int flags, form;
   long long sweep, z_begin;
+  int zr0, zr1;        // slab-local layers of this launch, [zr0, zr1) (K2: one per grid.x)
 };
 
 struct SweepParams {
   int nx, ny, zc, zchunk;
+  int zr0, zr1;        // slab-local layers this launch computes, [zr0, zr1) (partial re-execution)
   int64_t px;          // row pitch of the field buffers (elements)
   int64_t plane;       // layer pitch = px * ny
   int has_lo, has_hi;  // neighbour rank below / above (halo layers valid)

@@ -26,7 +26,8 @@ static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p) {
+cudaError_t launch_k2(int dtype, int shape, cudaStream_t s, const CheckParams& p) {
+  const int zc = p.zr1 - p.zr0;   // layers of this launch
   // one CTA per layer; few layers (cfg1-3 tiles): split each layer's entries
   // over up to 2 x SMs / zc CTAs, at least kCheckThreads entries each
   static int nsm = 0;
@@ -113,8 +114,8 @@ cudaError_t prime_checks(int dtype, int shape, int bc) {
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s) {
   FieldVal f{u, px, plane, dtype};
-  k0_colsum<<<dim3(zc, (nx + 255) / 256), 256, 0, s>>>(f, nx, ny, A, off);
-  k0_rowsum<<<dim3(zc, (ny + 127) / 128), 128, 0, s>>>(f, nx, ny, B, off);
+  k0_colsum<<<(unsigned)((int64_t)zc * ((nx + 255) / 256)), 256, 0, s>>>(f, dtype, nx, ny, A, off);
+  k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, B, off);
   return cudaGetLastError();
 }
 
@@ -122,14 +123,14 @@ cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, i
                             int nsources, int field_src, const double* coef, const double* scalar,
                             double* cA, double* cB, cudaStream_t s) {
   ConstVal f;
-  f.field = field; f.fpx = fpx; f.fplane = fpx * ny; f.dtype = dtype;
+  f.field = field_src >= 0 ? field : nullptr; f.fpx = fpx; f.fplane = fpx * ny; f.dtype = dtype;
   f.nsources = nsources; f.field_src = field_src;
   for (int q = 0; q < kMaxSources; ++q) {
     f.coef[q] = q < nsources ? coef[q] : 0.0;
     f.scalar[q] = q < nsources ? scalar[q] : 0.0;
   }
-  k0_colsum<<<dim3(zc, (nx + 255) / 256), 256, 0, s>>>(f, nx, ny, cA, 0);
-  k0_rowsum<<<dim3(zc, (ny + 127) / 128), 128, 0, s>>>(f, nx, ny, cB, 0);
+  k0_colsum<<<(unsigned)((int64_t)zc * ((nx + 255) / 256)), 256, 0, s>>>(f, dtype, nx, ny, cA, 0);
+  k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, cB, 0);
   return cudaGetLastError();
 }
 

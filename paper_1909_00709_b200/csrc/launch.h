@@ -48,7 +48,8 @@ ABFT_K1_DECL(launch_k1_f64_s4)
 ABFT_K1_DECL(launch_k1_f32_s3_ck0) ABFT_K1_DECL(launch_k1_f32_s3_ck1) ABFT_K1_DECL(launch_k1_f32_s3_ck2)
 ABFT_K1_DECL(launch_k1_f64_s3_ck0) ABFT_K1_DECL(launch_k1_f64_s3_ck1) ABFT_K1_DECL(launch_k1_f64_s3_ck2)
 #undef ABFT_K1_DECL
-cudaError_t launch_k2(int dtype, int shape, int zc, cudaStream_t s, const CheckParams& p);
+// K2 over the layers [p.zr0, p.zr1)
+cudaError_t launch_k2(int dtype, int shape, cudaStream_t s, const CheckParams& p);
 // fill n elements of a field buffer with v (constant ghost layers)
 cudaError_t launch_fill(int dtype, void* ptr, int64_t n, double v, cudaStream_t s);
 // load the check kernels of (dtype, shape, bc) now (CUDA lazy module loading)

@@ -357,6 +357,105 @@ __device__ __forceinline__ void stencil_layer_grouped(T (&out)[RY][16 / sizeof(T
   }
 }
 
+// Plane-streaming shapes: points sorted by (dk, dj, di) ascending, strictly
+// (the 27-point box of cfg5 and any radius-1 subset listed that way).
+template <class SH> __host__ __device__ constexpr bool sh_streamable() {
+  for (int q = 1; q < SH::NP; ++q) {
+    const int a = (SH::off(q - 1, 2) * 3 + SH::off(q - 1, 1)) * 3 + SH::off(q - 1, 0);
+    const int b = (SH::off(q, 2) * 3 + SH::off(q, 1)) * 3 + SH::off(q, 0);
+    if (a >= b) return false;
+  }
+  return true;
+}
+
+// One staged row t of a plane in registers: W[1..V] = the thread's vector,
+// W[0] / W[V+1] = its x neighbours (shuffles + one broadcast shared load),
+// with the boundary ghosts of an edge tile (clamp in x; constant / periodic
+// ghosts for every out-of-domain entry -- zero ghosts are the TMA's fill).
+// gplane: the plane in global memory (periodic wrap reads).
+template <typename T, bool EDGE, bool BCG>
+__device__ __forceinline__ void load_row(T (&W)[16 / sizeof(T) + 2], const unsigned char* slot, int sro,
+                                         int seo, int t, int lane, int gx0, int nx, const EdgeCtx<T>& ec,
+                                         const T* gplane) {
+  constexpr int V = 16 / (int)sizeof(T);
+  T c[V];
+  ld_vec<T, V>(c, reinterpret_cast<const T*>(slot + sro));
+#pragma unroll
+  for (int k = 0; k < V; ++k) W[k + 1] = c[k];
+  const T e = *reinterpret_cast<const T*>(slot + seo);
+  T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+  T right = __shfl_down_sync(0xffffffffu, c[0], 1);
+  W[0] = lane == 0 ? e : left;
+  W[V + 1] = lane == 31 ? e : right;
+  if constexpr (EDGE) {
+    if (ec.bc == ABFT_BC_CLAMP) {
+      if (gx0 == 0) W[0] = W[1];
+#pragma unroll
+      for (int c2 = 1; c2 < V + 2; ++c2)
+        if (gx0 - 1 + c2 >= nx) W[c2] = W[c2 - 1];
+    }
+  }
+  if constexpr (EDGE && BCG) {
+    if (ec.bc == ABFT_BC_CONSTANT || ec.bc == ABFT_BC_PERIODIC) {
+      const int gy = ec.gyb - 1 + t;
+      const bool yo = gy < 0 || gy >= ec.ny;
+#pragma unroll
+      for (int c2 = 0; c2 < V + 2; ++c2) {
+        const int gx = gx0 - 1 + c2;
+        if (yo || gx < 0 || gx >= nx) {
+          if (ec.bc == ABFT_BC_CONSTANT) {
+            W[c2] = ec.g;
+          } else {
+            const int wy = ((gy % ec.ny) + ec.ny) % ec.ny, wx = ((gx % nx) + nx) % nx;
+            W[c2] = gplane[(size_t)wy * ec.px + wx];
+          }
+        }
+      }
+    }
+  }
+}
+
+// Plane-streaming evaluation of Eq. 1 (streamable shapes, the 27-point box):
+// the staged plane q is read ONCE per thread and advances the FMA chains of
+// three outputs -- u^s[q + 1] (q is its dk = -1 plane: the chain's start, S),
+// u^s[q] (dk = 0: the middle, M) and u^s[q - 1] (dk = +1: the chain's end, E).
+// Its row t feeds output row r = t - 1 - dj, so the rows stream as well: one
+// staged row is live at a time.  Every output's chain still passes through
+// the points in their canonical order -- planes in ascending dk, rows in
+// ascending dj, di ascending -- so the result is bitwise that of the
+// three-plane evaluation, while each staged element is
+// loaded (and its x halo exchanged) once instead of three times.
+// de / dm / ds: which of the three chains exist (chunk ends; RT = false: all
+// three, the steady state, without the runtime tests).
+template <typename T, class SH, int RY, bool EDGE, bool BCG, bool RT>
+__device__ __forceinline__ void stream_plane(T (&ae)[RY][16 / sizeof(T)], T (&am)[RY][16 / sizeof(T)],
+                                             T (&as)[RY][16 / sizeof(T)], bool de, bool dm, bool ds,
+                                             const unsigned char* slot, const RowOffs<RY>& ro,
+                                             const SweepParams& p, int lane, int gx0, int nx,
+                                             const EdgeCtx<T>& ec, const T* gplane) {
+  constexpr int V = 16 / (int)sizeof(T), NP = SH::NP;
+#pragma unroll
+  for (int t = 0; t < RY + 2; ++t) {
+    T W[V + 2];
+    load_row<T, EDGE, BCG>(W, slot, ro.sro[t], ro.seo[t], t, lane, gx0, nx, ec, gplane);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int di = SH::off(q, 0), dj = SH::off(q, 1), dk = SH::off(q, 2);
+      const int r = t - 1 - dj;
+      if (r < 0 || r >= RY) continue;
+      if (RT && ((dk < 0 && !ds) || (dk == 0 && !dm) || (dk > 0 && !de))) continue;
+      T (&acc)[RY][V] = dk < 0 ? as : (dk == 0 ? am : ae);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const T v = W[k + 1 + di];
+        // the weight is read from the parameter bank at its use (27 fp64
+        // weights in registers would crowd out the three chains)
+        acc[r][k] = (q == 0) ? mul_rn(pw<T>(p, q), v) : fma_rn(pw<T>(p, q), v, acc[r][k]);
+      }
+    }
+  }
+}
+
 template <typename T, class SH, int RY, bool NZ, bool EDGE, bool BCG = true>
 __device__ __forceinline__ void stencil_layer(T (&out)[RY][16 / sizeof(T)], const T* const (&pl)[3],
                                               const RowOffs<RY>& ro, const T (&wr)[SH::NP],
@@ -435,6 +534,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   constexpr int SS = GEN ? SHAPE_HOTSPOT7 : S;   // any defined shape for the GEN instantiation
   constexpr bool NZ = GEN ? true : shape_needs_z<SS>();
   constexpr int NP = GEN ? 1 : Shape<SS>::NP;
+  constexpr bool STREAM = !GEN && sh_streamable<Shape<SS>>();   // plane streaming (27-point box)
 
   // shared memory: derived from the __shared__ array so every access is LDS/STS
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -446,7 +546,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = p.nx, ny = p.ny, zc = p.zc;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int zs = blockIdx.z * p.zchunk, ze = min(zs + p.zchunk, zc);
+  const int zs = p.zr0 + blockIdx.z * p.zchunk, ze = min(zs + p.zchunk, p.zr1);
   const int q0 = NZ ? zs - 1 : zs;
   const int nT = (NZ ? ze + 1 : ze) - q0;
   const bool hasP = p.field_src >= 0;
@@ -512,7 +612,7 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     if (full) load_src<T, RY, true>(dst, q, p.spx, gyb, gx0, nx, ny);
     else load_src<T, RY, false>(dst, q, p.spx, gyb, gx0, nx, ny);
   };
-  if (hasP) src_layer(pa, psrc);
+  if (hasP && !STREAM) src_layer(pa, psrc);
   // output row of this thread in layer zs (buffer layer zs + 1), advanced per layer
   T* orow = out_base + (size_t)(zs + 1) * p.plane + (size_t)gyb * px + gx0;
   const RowOffs<RY> ro = row_offsets<T, RY>(srow, lane);
@@ -525,69 +625,10 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     if (final_lane<RY>(lane) && gy < ny) atomicAdd(&Bg[(size_t)(zl + 1) * ny + gy], tot);
   };
   (void)flush_rows;
-  auto layer = [&](const int z, T (&pv)[RY][V], T (&pn)[RY][V]) {
+  // per output layer z: the sources C, the flips, the store, the halo and
+  // ledger copies, the checksums (Eqs. 2-3) and the ring barrier
+  auto epilogue = [&](const int z, T (&out)[RY][V], const T (&pv)[RY][V]) {
     const int it = z - zs;
-    const T* pl[3];
-    if (NZ) {
-      // entries it, it+1 were waited for by the previous layer (or here, first)
-      if (it == 0) {
-        mbar_wait(&barT[0], 0);
-        mbar_wait(&barT[1 % NS], (1 / NS) & 1);
-      }
-      mbar_wait(&barT[(it + 2) % NS], ((it + 2) / NS) & 1);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) pl[d] = sT + ((it + d) % NS) * TSTR;
-    } else {
-      mbar_wait(&barT[it % NS], (it / NS) & 1);
-      pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
-    }
-    if (hasP && z + 1 < ze) src_layer(pn, psrc + (size_t)(it + 1) * p.splane);
-
-    T out[RY][V];
-    if constexpr (!GEN) {
-      // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
-      if (edge) {
-        if constexpr (GEN_BC) {
-          const T* ub = reinterpret_cast<const T*>(p.uin);
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            ec.up[d] = ub + (size_t)(NZ ? zmap(z - 1 + d, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
-        }
-        stencil_layer<T, Shape<SS>, RY, NZ, true, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
-      } else {
-        stencil_layer<T, Shape<SS>, RY, NZ, false, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
-      }
-    } else {
-      // generic radius-1 point list: runtime offsets, identical FMA chain
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          T acc = T(0);
-          for (int q = 0; q < p.npoints; ++q) {
-            const int di = p.di[q], dj = p.dj[q], dk = p.dk[q];
-            const T* pp = dk < 0 ? pl[0] : (dk > 0 ? pl[2] : pl[1]);
-            const int yy = gyb + r + dj, xx = gx0 + k + di;
-            T v;
-            if (bc == ABFT_BC_CLAMP || (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ||
-                (!GEN_BC && bc != ABFT_BC_ZERO)) {
-              const int sr = (max(0, min(yy, ny - 1)) - y0 + 1) * HX;
-              const int sc = max(0, min(xx, nx - 1)) - x0 + HV;
-              v = pp[sr + sc];
-            } else if (bc == ABFT_BC_PERIODIC) {
-              const T* ub = reinterpret_cast<const T*>(p.uin) +
-                            (size_t)(NZ ? zmap(z + dk, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
-              v = ub[(size_t)(((yy % ny) + ny) % ny) * px + ((xx % nx) + nx) % nx];
-            } else {
-              v = bc == ABFT_BC_CONSTANT ? (T)p.g : T(0);
-            }
-            const T w = pw<T>(p, q);
-            acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
-          }
-          out[r][k] = acc;
-        }
-      }
-    }
 #if ABFT_ROWS_DEFERRED
     if constexpr (CHK != K1_CK_NONE) {
       if (zprev >= 0) flush_rows(zprev);   // b of the previous layer (Eq. 3)
@@ -719,12 +760,123 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       }
     }
   };
-  int z = zs;
-  for (; z + 1 < ze; z += 2) {
-    layer(z, pa, pb);
-    layer(z + 1, pb, pa);
+  auto layer = [&](const int z, T (&pv)[RY][V], T (&pn)[RY][V]) {
+    const int it = z - zs;
+    const T* pl[3];
+    if (NZ) {
+      // entries it, it+1 were waited for by the previous layer (or here, first)
+      if (it == 0) {
+        mbar_wait(&barT[0], 0);
+        mbar_wait(&barT[1 % NS], (1 / NS) & 1);
+      }
+      mbar_wait(&barT[(it + 2) % NS], ((it + 2) / NS) & 1);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) pl[d] = sT + ((it + d) % NS) * TSTR;
+    } else {
+      mbar_wait(&barT[it % NS], (it / NS) & 1);
+      pl[0] = pl[2] = pl[1] = sT + (it % NS) * TSTR;
+    }
+    if (hasP && z + 1 < ze) src_layer(pn, psrc + (size_t)(it + 1) * p.splane);
+
+    T out[RY][V];
+    if constexpr (!GEN) {
+      // CTA-uniform split: only tiles touching x = 0 / x = nx - 1 pay the clamp
+      if (edge) {
+        if constexpr (GEN_BC) {
+          const T* ub = reinterpret_cast<const T*>(p.uin);
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            ec.up[d] = ub + (size_t)(NZ ? zmap(z - 1 + d, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
+        }
+        stencil_layer<T, Shape<SS>, RY, NZ, true, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
+      } else {
+        stencil_layer<T, Shape<SS>, RY, NZ, false, GEN_BC>(out, pl, ro, wr, lane, gx0, nx, ec);
+      }
+    } else {
+      // generic radius-1 point list: runtime offsets, identical FMA chain
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          T acc = T(0);
+          for (int q = 0; q < p.npoints; ++q) {
+            const int di = p.di[q], dj = p.dj[q], dk = p.dk[q];
+            const T* pp = dk < 0 ? pl[0] : (dk > 0 ? pl[2] : pl[1]);
+            const int yy = gyb + r + dj, xx = gx0 + k + di;
+            T v;
+            if (bc == ABFT_BC_CLAMP || (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ||
+                (!GEN_BC && bc != ABFT_BC_ZERO)) {
+              const int sr = (max(0, min(yy, ny - 1)) - y0 + 1) * HX;
+              const int sc = max(0, min(xx, nx - 1)) - x0 + HV;
+              v = pp[sr + sc];
+            } else if (bc == ABFT_BC_PERIODIC) {
+              const T* ub = reinterpret_cast<const T*>(p.uin) +
+                            (size_t)(NZ ? zmap(z + dk, zc, p.has_lo, p.has_hi, bc) : z + 1) * p.plane;
+              v = ub[(size_t)(((yy % ny) + ny) % ny) * px + ((xx % nx) + nx) % nx];
+            } else {
+              v = bc == ABFT_BC_CONSTANT ? (T)p.g : T(0);
+            }
+            const T w = pw<T>(p, q);
+            acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
+          }
+          out[r][k] = acc;
+        }
+      }
+    }
+    epilogue(z, out, pv);
+  };
+  if constexpr (STREAM) {
+    // plane streaming (the 27-point box): staged plane q
+    // advances the chains of u^s[q + 1], u^s[q] and u^s[q - 1] (stream_plane);
+    // three accumulator sets rotate through the roles start / middle / end
+    (void)layer;
+    // E: u^s[z] (start and middle done), M: u^s[z + 1] (start done), S: u^s[z + 2];
+    // after each layer the roles rotate by register moves (E <- M <- S), so
+    // the loop body holds one copy of the plane code (instruction cache)
+    T E[RY][V], M[RY][V], S[RY][V];
+    const T* ub = reinterpret_cast<const T*>(p.uin);
+    auto splane = [&](int i, bool rt, bool de, bool dm, bool ds) {
+      mbar_wait(&barT[i % NS], (i / NS) & 1);   // ring slot i holds plane q0 + i
+      const unsigned char* slot = reinterpret_cast<const unsigned char*>(sT + (i % NS) * TSTR);
+      const T* gpl = GEN_BC ? ub + (size_t)zmap(q0 + i, zc, p.has_lo, p.has_hi, bc) * p.plane : nullptr;
+      using SHP = Shape<SS>;
+      if (rt) {
+        if (edge) stream_plane<T, SHP, RY, true, GEN_BC, true>(E, M, S, de, dm, ds, slot, ro, p, lane, gx0, nx, ec, gpl);
+        else stream_plane<T, SHP, RY, false, GEN_BC, true>(E, M, S, de, dm, ds, slot, ro, p, lane, gx0, nx, ec, gpl);
+      } else {
+        if (edge) stream_plane<T, SHP, RY, true, GEN_BC, false>(E, M, S, de, dm, ds, slot, ro, p, lane, gx0, nx, ec, gpl);
+        else stream_plane<T, SHP, RY, false, GEN_BC, false>(E, M, S, de, dm, ds, slot, ro, p, lane, gx0, nx, ec, gpl);
+      }
+    };
+    auto rotate = [&]() {
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int k = 0; k < V; ++k) { E[r][k] = M[r][k]; M[r][k] = S[r][k]; }
+    };
+    // prologue: plane zs - 1 starts u^s[zs] (its only role here); plane zs
+    // continues u^s[zs] and starts u^s[zs + 1] -- each as if it ended the
+    // layer before, then the roles rotate
+    splane(0, true, false, false, true);
+    rotate();
+    splane(1, true, false, true, zs + 1 < ze);
+    rotate();
+#pragma unroll 1
+    for (int z = zs; z < ze; ++z) {
+      T pv[RY][V];
+      if (hasP) src_layer(pv, psrc + (size_t)(z - zs) * p.splane);
+      splane(z - zs + 2, z + 2 >= ze, true, z + 1 < ze, z + 2 < ze);   // plane z + 1 ends u^s[z]
+      epilogue(z, E, pv);
+      rotate();
+    }
+  } else {
+    int z = zs;
+    for (; z + 1 < ze; z += 2) {
+      layer(z, pa, pb);
+      layer(z + 1, pb, pa);
+    }
+    if (z < ze) layer(z, pa, pb);
   }
-  if (z < ze) layer(z, pa, pb);
 #if ABFT_ROWS_DEFERRED
   if constexpr (CHK != K1_CK_NONE) {
     if (zprev >= 0) flush_rows(zprev);

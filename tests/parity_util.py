@@ -87,13 +87,25 @@ def assert_field_equal(g, o, dtype):
 
 
 def assert_checksums_close(g, o, rtol):
+    """a (sums over y) and b (sums over x) of the final field.  fp32 data in
+    the configs' ranges sum exactly in fp64, so any summation order gives the
+    same bits (rtol 0).  Where a sum is not exact -- an uncorrected exponent
+    flip leaves a cell ~1e21 in the layer, or fp64 data -- the GPU's
+    reduction order and the oracle's ascending order may round differently;
+    both lie within the textbook bound (n - 1) 2^-53 sum|u| of the exact sum
+    (DESIGN.md "Parity bars"), so they may differ by twice that."""
+    u = np.abs(o["u"].astype(np.float64))
+    bound = {"A": 2.0 * u.shape[1] * 2.0 ** -53 * u.sum(axis=1),
+             "B": 2.0 * u.shape[2] * 2.0 ** -53 * u.sum(axis=2)}
     for k in ("A", "B"):
         a, b = g[k], o[k]
+        same = (a == b) | (np.isnan(a) & np.isnan(b))
         if rtol == 0.0:
-            assert np.array_equal(a, b), (k, np.flatnonzero(a != b)[:10])
+            bad = ~same & ~(np.abs(a - b) <= bound[k])
         else:
             rel = np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
-            assert rel.max() <= rtol, (k, rel.max())
+            bad = ~same & ~(rel <= rtol) & ~(np.abs(a - b) <= bound[k])
+        assert not bad.any(), (k, np.flatnonzero(bad)[:10], a[bad][:3], b[bad][:3])
 
 
 def parity(p, nsweeps=None, faults=None, explicit=False, dtype=None, **kw):

@@ -5,6 +5,7 @@ header documents.  No compute call is made here."""
 import ctypes as C
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -36,13 +37,20 @@ def test_library_exports_every_declared_symbol(L):
         assert hasattr(L, name), name
 
 
-def test_struct_sizes_match_header_layout():
-    assert C.sizeof(abft.abft_point) == 24
-    assert C.sizeof(abft.abft_source) == 24
-    assert C.sizeof(abft.abft_fault) == 40
-    assert C.sizeof(abft.abft_record) == 80
-    assert C.sizeof(abft.abft_stats) == 72
-    assert C.sizeof(abft.abft_config) == 120
+def test_struct_sizes_match_header_layout(tmp_path):
+    # the ctypes mirrors against the header itself, compiled with gcc
+    src = tmp_path / "sz.c"
+    names = ["abft_point", "abft_source", "abft_fault", "abft_record", "abft_stats", "abft_config"]
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "abft_stencil.h"\nint main(void){'
+                   + "".join(f'printf("%zu\\n", sizeof({n}));' for n in names)
+                   + 'printf("%zu\\n", offsetof(abft_config, recovery));return 0;}\n')
+    exe = tmp_path / "sz"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert got[:-1] == [C.sizeof(getattr(abft, n)) for n in names]
+    assert got[-1] == abft.abft_config.recovery.offset
 
 
 def test_strerror(L):
@@ -85,6 +93,7 @@ def test_workspace_size_sane(L):
     (dict(bc=abft.ABFT_BC_CONSTANT, bc_value=float("inf")), abft.ABFT_EINVAL),
     (dict(bc=9), abft.ABFT_EINVAL),
     (dict(checksum_policy=2), abft.ABFT_EINVAL),
+    (dict(recovery=2), abft.ABFT_EINVAL),
     (dict(z_begin=1, z_count=2), abft.ABFT_EINVAL),
     (dict(nranks=2, rank=1, z_count=2), abft.ABFT_EINVAL),   # rank 1 cannot own layer 0
     (dict(nranks=2, rank=0, z_count=4), abft.ABFT_EINVAL),   # rank 0 of 2 owns every layer

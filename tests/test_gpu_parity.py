@@ -518,3 +518,53 @@ def test_multi_flip_layer_uncorrectable_and_unlocated(form, checksums):
     q = make_problem("cfg2", nx=8, ny=1024, nz=3, sweeps=4, correction_form=form, checksums=checksums)
     g, o = parity(q, faults=[Fault(2, 1, 500, 3, 12)])
     assert [r["status"] for r in o["records"]] == [abft.REC_UNLOCATED]
+
+
+# ---- offline partial re-execution (recovery PARTIAL, Q28) ---------
+
+@pytest.mark.parametrize("delta", [1, 3, 6])
+def test_offline_partial_reexecution_equals_oracle(delta):
+    p = make_problem("cfg3", nx=96, ny=80, nz=40, sweeps=4 * delta, mode=2, delta=delta, recovery=1)
+    faults = [Fault(1, 11, 7, 9, 24), Fault(delta + 1, 0, 79, 95, 30), Fault(2 * delta + 1, 39, 0, 0, 28),
+              Fault(3 * delta + 1, 5, 20, 20, 24), Fault(3 * delta + 1, 30, 3, 30, 29),
+              Fault(4 * delta, 20, 40, 50, 3)]
+    g, o = parity(p, faults=faults)
+    assert o["stats"]["rollbacks"] == 4
+    ref = gpu_run(p.replace(recovery=0), faults=faults)
+    assert ref["stats"]["sweeps"] == g["stats"]["sweeps"]
+
+
+def test_offline_partial_keeps_undetected_error_outside_the_cone():
+    p = make_problem("cfg3", nx=40, ny=32, nz=24, sweeps=4, mode=2, delta=4, recovery=1)
+    faults = [Fault(1, 2, 5, 5, 29), Fault(1, 20, 9, 9, 3)]
+    g, o = parity(p, faults=faults)
+    only_lo = gpu_run(p, faults=[faults[1]])
+    assert np.array_equal(g["u"].view(np.uint32), only_lo["u"].view(np.uint32))
+
+
+def test_offline_partial_persistent_error():
+    p = make_problem("cfg3", nx=32, ny=32, nz=10, sweeps=10, mode=2, delta=5, recovery=1)
+    g, o = parity(p, faults=[Fault(3, 1, 5, 5, 30), Fault(3, 1, 5, 5, 30)])
+    assert o["status"] == 3 and o["stats"]["persistent"] == 1
+
+
+def test_offline_partial_fp64_box27():
+    p = make_problem("cfg5", nx=130, ny=67, nz=30, sweeps=20, nfaults=6, recovery=1)
+    g, o = parity(p)
+    assert o["stats"]["rollbacks"] >= 1
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_offline_partial_slab_group(G, halo):
+    # the cone crosses slab faces: re-execution, halos and the re-check are collective
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=24, sweeps=18, mode=2, delta=6, recovery=1)
+    faults = [Fault(1, 11, 7, 9, 24), Fault(7, 0, 79, 95, 30), Fault(13, 23, 0, 0, 28), Fault(13, 5, 5, 5, 29)]
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, G, faults)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+    assert np.array_equal(g["A"], o["A"]) and np.array_equal(g["B"], o["B"])
+    for s in g["stats"]:
+        for k in ("sweeps", "rollbacks", "windows", "persistent"):
+            assert s[k] == o["stats"][k], (k, s, o["stats"])

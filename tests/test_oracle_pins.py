@@ -586,3 +586,51 @@ def test_offline_interpolation_matches_direct_after_delta_sweeps():
         u = O.sweep(op, u)
     A1, B1 = _fsum_checksums(u)
     assert np.max(np.abs(A - A1) / A1) < 1e-12 and np.max(np.abs(B - B1) / B1) < 1e-12
+
+
+# ------------------------------------- offline partial re-execution (Q28)
+
+def _offline(p, faults, recovery):
+    q = p.replace(recovery=recovery)
+    op = O.OProblem(q, [field_power(q).numpy()] if q.power else [])
+    return O.run(op, field_u0(q).numpy(), q.sweeps, faults)
+
+
+@pytest.mark.parametrize("delta", [1, 3, 6])
+def test_partial_reexecution_of_detected_errors_restores_the_fault_free_run(delta):
+    # stencil locality: re-executing only the light
+    # cone of the flagged layers erases every detected error, so the result
+    # is the fault-free run bitwise -- like the full rollback.  Flips
+    # at a window's first sweep spread over the whole window; bit 24 of a
+    # value ~333 (delta ~1e3) flags its own layer while the layers it reaches
+    # 3+ sweeps later stay below eps: a cone of the flagged layers alone
+    # (no 2(L - 1) margin) would leave those errors in place.
+    p = make_problem("cfg3", nx=48, ny=40, nz=24, sweeps=4 * delta, mode=2, delta=delta)
+    ref = _offline(p, [], 0)
+    faults = [Fault(1, 11, 7, 9, 24), Fault(delta + 1, 0, 39, 47, 30),
+              Fault(2 * delta + 1, 23, 0, 0, 28), Fault(3 * delta + 1, 5, 20, 20, 24),
+              Fault(3 * delta + 1, 17, 3, 30, 29)]
+    for recovery in (0, 1):
+        r = _offline(p, faults, recovery)
+        assert r["stats"]["rollbacks"] == 4 and r["stats"]["persistent"] == 0 and r["status"] == 0
+        assert r["stats"]["sweeps"] == 8 * delta
+        assert (r["u"].view(np.uint32) == ref["u"].view(np.uint32)).all()
+        assert np.array_equal(r["A"], ref["A"]) and np.array_equal(r["B"], ref["B"])
+
+
+def test_partial_reexecution_keeps_layers_no_detected_error_reached():
+    # a detected flip in layer 2 and, in the same window, an undetected
+    # low-bit flip in layer 20: the full rollback erases both; the partial
+    # re-execution (window of 4 sweeps: cone 2 * 3 layers around layer 2)
+    # re-executes layers 0..8 only, so the result equals the run with the
+    # undetected flip alone
+    p = make_problem("cfg3", nx=40, ny=32, nz=24, sweeps=4, mode=2, delta=4)
+    hi, lo = Fault(1, 2, 5, 5, 29), Fault(1, 20, 9, 9, 3)
+    full = _offline(p, [hi, lo], 0)
+    part = _offline(p, [hi, lo], 1)
+    only_lo = _offline(p, [lo], 0)
+    clean = _offline(p, [], 0)
+    assert only_lo["stats"]["rollbacks"] == 0          # the low bit goes undetected
+    assert (full["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+    assert (part["u"].view(np.uint32) == only_lo["u"].view(np.uint32)).all()
+    assert not (part["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
