@@ -8,7 +8,8 @@ actual checksums, Eqs. 2-3) and K2 (Theorem 1 prediction, compare, locate,
 correct) over every z-layer, with the config's scheduled bit-flips.  The
 default workload is BASELINE.json configs[3] (cfg4): HotSpot3D 7-point,
 1024^3 fp32, online ABFT, 200 sweeps, one flip per 128-layer slab per 50
-sweeps, z-partitioned over N GPUs (one process per GPU, NCCL halo).  Inputs
+sweeps, z-partitioned over N GPUs (one process per GPU; the kernels store the
+halo into the neighbours' buffers over CUDA IPC, or NCCL send/recv).  Inputs
 (4 GiB per array) are larger than L2, so no flush is needed between steps.
 
 Prints ONE JSON line (rank 0).  `value` = protected GCell-updates/s of the
@@ -184,16 +185,30 @@ def run_ours(a):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
+    # N > 1: the z-slab halo moves over CUDA IPC by default -- the kernels store
+    # it into the neighbours' mapped buffers (fused halo, NVLink); with
+    # ABFT_TRANSPORT=nccl the library posts NCCL send/recv after each sweep
+    # instead, every handle of this process sharing one communicator (the
+    # library caches it by the unique id broadcast once here)
+    transport = os.environ.get("ABFT_TRANSPORT", "ipc") if world > 1 else "none"
+    ipc_ctx, nccl_id = None, None
+    if transport == "ipc":
+        from paper_1909_00709_b200.ipc import IpcContext
+        ipc_ctx = IpcContext(rank, world)
+    elif transport == "nccl":
+        import torch.distributed as dist
+        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
     def handle_kw():
-        # every handle gets its own communicator, so a fresh ncclUniqueId from
-        # rank 0 (an id is good for one ncclCommInitRank rendezvous)
-        nccl_id = None
-        if world > 1:
-            import torch.distributed as dist
-            obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nccl_id = obj[0]
         return dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
+
+    def new_handle(*args, **kw):
+        st = abft.from_problem(*args, **kw, **handle_kw())
+        if ipc_ctx is not None:
+            ipc_ctx.link(st)       # collective: every rank creates its handles in lockstep
+        return st
     p = make_problem(a.config)
     if not a.strong:            # weak scaling: each rank owns a slab of the config's size
         per = a.nz_per_gpu or (128 if a.config == "cfg5" else p.nz)
@@ -214,8 +229,7 @@ def run_ours(a):
     clocks = Clocks(idx)
 
     def protected_run(mode, with_faults, prof=False, policy=pol):
-        st = abft.from_problem(p, u0, P, device=dev, stream=stream, mode=mode,
-                               checksum_policy=policy, **handle_kw())
+        st = new_handle(p, u0, P, device=dev, stream=stream, mode=mode, checksum_policy=policy)
         if with_faults:
             st.set_faults(shift(faults, W))
         st.step(W)
@@ -304,8 +318,7 @@ def run_ours(a):
         def job():
             if Pd is not None:
                 Pd.copy_(Ph, non_blocking=True)
-            st = abft.from_problem(p, u0h, Pd, device=dev, stream=stream, checksum_policy=pol,
-                                   **handle_kw())
+            st = new_handle(p, u0h, Pd, device=dev, stream=stream, checksum_policy=pol)
             st.set_faults(faults)
             st.step(K)
             st.read_field(outh)
@@ -346,7 +359,8 @@ def run_ours(a):
                                            "(PAPER.md:271-273, 496-497)") if pol == abft.ABFT_CK_LAZY
                        else "both: a and b every sweep in the K1 pass",
                        "nx": p.nx, "ny": p.ny, "nz": p.nz, "z_per_gpu": zc,
-                       "parallelism": f"z-slab x{world} (NCCL halo)" if world > 1 else "1 GPU",
+                       "parallelism": (f"z-slab x{world} ({'CUDA IPC fused halo' if transport == 'ipc' else 'NCCL halo'})"
+                                       if world > 1 else "1 GPU"),
                        "l2": "inputs larger than L2 (4 GiB per array); no flush",
                        "k1_grid": list(prof["grid"]), "k1_threads": prof["threads"],
                        "k1_smem": prof["smem"], "k1_layers_per_cta": prof["zchunk"]},
@@ -378,6 +392,8 @@ def run_ours(a):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if ipc_ctx is not None:
+        ipc_ctx.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -247,6 +247,47 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n);
 int abft_stencil_halo_plan(const abft_config* cfg, int32_t plan[6]);
 int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps);
 
+/* Multi-process job over CUDA IPC (one process per slab and GPU, or several
+ * processes sharing a GPU): the fused halo of local groups across processes
+ * (the paper's distributed-memory claim).  Each rank
+ * creates its handle with cfg.nranks = n, cfg.rank = its rank and
+ * cfg.nccl_unique_id = NULL, then
+ *   1. abft_stencil_ipc_export(h, blob): writes ABFT_IPC_BLOB_BYTES describing
+ *      its buffers (cudaIpcMemHandle + offset of each field buffer and of aux,
+ *      the aux layout) and two interprocess events; synchronises the handle's
+ *      stream (its initial state is ready for the neighbours to read);
+ *   2. the blobs travel to the neighbours by any host channel (bench.py and the
+ *      tests use torch.distributed all_gather_object);
+ *   3. abft_stencil_ipc_link(h, lo_blob, hi_blob, shm): maps the neighbours'
+ *      buffers (peer access over NVLink, or the same GPU), opens their events,
+ *      pulls the initial halo and zeroes this rank's progress slot.  lo_blob /
+ *      hi_blob: the blob of rank - 1 / rank + 1, NULL at a global face.  shm:
+ *      an array of nranks abft_ipc_slot in host memory mapped by every
+ *      process of the job (e.g. a /dev/shm segment), zero-initialised; the
+ *      caller keeps it mapped until destroy.  Every rank must have linked (a
+ *      barrier) before any rank steps.
+ * Then step() stores each sweep's boundary layers, their checksum (or
+ * prediction) rows and any correction of a boundary cell straight into the
+ * neighbours' halo slots from K1 / K2 / K3, and orders the next sweep after
+ * the neighbours' through the events (a rank publishes its sweep count in
+ * its slot; a neighbour enqueues the wait once the count is there).  Offline
+ * window verdicts and the extent of the flagged layers (partial
+ * re-execution) are reduced over all ranks through the slots.  Every rank
+ * calls step() with the same counts (lockstep).  Errors: ABFT_EINVAL for a
+ * handle that is grouped, has a communicator, has stepped, or a blob that
+ * does not describe the expected neighbour; ABFT_ECUDA if a handle or event
+ * cannot be opened. */
+#define ABFT_IPC_BLOB_BYTES 1024
+typedef struct {
+  int64_t seq;        /* halo exchanges this rank has published */
+  int64_t wseq;       /* offline windows whose verdict this rank has published */
+  int64_t wdone;      /* offline windows this rank has reduced */
+  int32_t val[2][3];  /* verdict per window parity: flagged layers, extent words */
+  int32_t pad[2];
+} abft_ipc_slot;
+int abft_stencil_ipc_export(abft_stencil* h, void* blob);
+int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_blob, void* shm);
+
 /* Explicit-control API (ONLINE / NONE handles), the paper's listings one by
  * one.  sweep(): one sweep with the actual checksums of the result (fig.sweep).
  * check(): predicted checksums of the last sweep (Theorem 1, fig.interpolation)
@@ -259,9 +300,11 @@ int abft_stencil_check(abft_stencil* h, int64_t* nflag_a, int64_t* nflag_b);
 int abft_stencil_correct(abft_stencil* h, int64_t* ncorrected);
 
 /* Schedule bit-flips (test / measurement hook).  Replaces the pending list;
- * faults outside this rank's slab are ignored by this rank.  ABFT_EINVAL (and
- * an empty list) if a fault is out of range, two faults hit the same cell in
- * the same sweep, or more than 64 fall in this slab in one sweep. */
+ * faults outside this rank's slab are ignored by this rank.  A cell listed k
+ * times for one sweep is flipped in k executions of that sweep (the first and
+ * k - 1 offline re-executions: a fault that strikes again, i.e. a persistent
+ * error).  ABFT_EINVAL (and an empty list) if a fault is out of range or more
+ * than 64 entries fall in this slab in one sweep. */
 int abft_stencil_set_faults(abft_stencil* h, const abft_fault* faults, int32_t n);
 
 /* Read-back.  All synchronise the handle's stream. */

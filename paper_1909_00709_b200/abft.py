@@ -32,7 +32,8 @@ EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_ste
            "abft_stencil_status", "abft_stencil_sweep_count", "abft_stencil_launch_count",
            "abft_stencil_destroy", "abft_strerror", "abft_stencil_profile",
            "abft_stencil_profile_read", "abft_stencil_group", "abft_stencil_step_group",
-           "abft_stencil_halo_plan")
+           "abft_stencil_halo_plan", "abft_stencil_ipc_export", "abft_stencil_ipc_link")
+IPC_BLOB_BYTES = 1024
 
 
 class abft_point(C.Structure):
@@ -72,6 +73,11 @@ class abft_stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("sweeps", "detections", "located", "corrected",
                                          "unlocated", "uncorrectable", "rollbacks", "windows",
                                          "persistent")]
+
+
+class abft_ipc_slot(C.Structure):
+    _fields_ = [("seq", C.c_int64), ("wseq", C.c_int64), ("wdone", C.c_int64),
+                ("val", (C.c_int32 * 3) * 2), ("pad", C.c_int32 * 2)]
 
 
 class AbftError(RuntimeError):
@@ -119,6 +125,8 @@ def lib() -> C.CDLL:
         L.abft_stencil_halo_plan.argtypes = [cfgp, C.POINTER(i32)]
         L.abft_stencil_group.argtypes = [C.POINTER(vp), i32]
         L.abft_stencil_step_group.argtypes = [C.POINTER(vp), i32, i32]
+        L.abft_stencil_ipc_export.argtypes = [vp, vp]
+        L.abft_stencil_ipc_link.argtypes = [vp, vp, vp, vp]
         L.abft_strerror.argtypes = [C.c_int]
         L.abft_strerror.restype = C.c_char_p
         _lib = L
@@ -337,6 +345,21 @@ class Stencil:
             self.destroy()
         except Exception:
             pass
+
+
+def ipc_export(st: Stencil) -> bytes:
+    """abft_stencil_ipc_export: this slab's IPC description for its neighbours."""
+    buf = C.create_string_buffer(IPC_BLOB_BYTES)
+    _ok("abft_stencil_ipc_export", lib().abft_stencil_ipc_export(st.h, buf))
+    return buf.raw
+
+
+def ipc_link(st: Stencil, lo_blob: Optional[bytes], hi_blob: Optional[bytes], shm_addr: int) -> None:
+    """abft_stencil_ipc_link: map the neighbours' buffers and events; shm_addr
+    is the address of nranks abft_ipc_slot shared by every process of the job."""
+    lo = C.create_string_buffer(lo_blob, IPC_BLOB_BYTES) if lo_blob is not None else None
+    hi = C.create_string_buffer(hi_blob, IPC_BLOB_BYTES) if hi_blob is not None else None
+    _ok("abft_stencil_ipc_link", lib().abft_stencil_ipc_link(st.h, lo, hi, C.c_void_p(shm_addr)))
 
 
 def _handles(stencils):

@@ -7,6 +7,9 @@
 // sequences launches on the caller's stream.  There is no CPU fallback: a
 // missing device or driver entry point is a hard ABFT_ECUDA.
 #include <dlfcn.h>
+#include <sched.h>
+#include <map>
+#include <array>
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
@@ -58,6 +61,45 @@ NcclApi* nccl_api() {
   api.ok = api.commInitRank && api.commDestroy && api.groupStart && api.groupEnd && api.send &&
            api.recv && api.allReduce;
   return api.ok ? &api : nullptr;
+}
+
+// One communicator per (job, rank): handles created with the same unique id
+// share it (reference counted), so a process that runs several handles of one
+// job in turn -- bench.py's runs -- pays one ncclCommInitRank.  Handles that
+// share a communicator must not run concurrently.
+struct CommCache {
+  std::map<std::array<char, sizeof(ncclUniqueId)>, std::pair<ncclComm_t, int>> m;
+};
+CommCache& comm_cache() {
+  static CommCache c;
+  return c;
+}
+int comm_acquire(const void* id_bytes, int nranks, int rank, ncclComm_t* out) {
+  NcclApi* n = nccl_api();
+  if (!n) return ABFT_ENCCL;
+  std::array<char, sizeof(ncclUniqueId)> key;
+  memcpy(key.data(), id_bytes, key.size());
+  auto it = comm_cache().m.find(key);
+  if (it != comm_cache().m.end()) {
+    it->second.second++;
+    *out = it->second.first;
+    return ABFT_OK;
+  }
+  ncclUniqueId id;
+  memcpy(&id, id_bytes, sizeof(id));
+  if (n->commInitRank(out, nranks, id, rank) != ncclSuccess) return ABFT_ENCCL;
+  comm_cache().m[key] = {*out, 1};
+  return ABFT_OK;
+}
+void comm_release(ncclComm_t c) {
+  for (auto it = comm_cache().m.begin(); it != comm_cache().m.end(); ++it)
+    if (it->second.first == c) {
+      if (--it->second.second == 0) {
+        if (NcclApi* n = nccl_api()) n->commDestroy(c);
+        comm_cache().m.erase(it);
+      }
+      return;
+    }
 }
 
 // ------------------------------------------------------- TMA descriptor encode
@@ -244,6 +286,15 @@ struct abft_stencil {
   int host_worst = 0;
   std::vector<PendingFault> faults;
   ncclComm_t comm = nullptr;
+  // multi-process job over CUDA IPC (abft_stencil_ipc_link): neighbour proxies
+  // (mapped buffers + IPC events), the host-shared progress slots, counters
+  bool ipc = false;
+  abft_ipc_slot* shm = nullptr;
+  int64_t xseq = 0, wseq = 0;
+  cudaEvent_t ev_ipc[2] = {nullptr, nullptr};
+  std::vector<void*> ipc_opened;   // bases from cudaIpcOpenMemHandle (closed at destroy)
+  abft_stencil* proxy[2] = {nullptr, nullptr};
+  bool is_proxy = false;
   int has_lo = 0, has_hi = 0;
   // local group (several slabs in one process): neighbours and sync events
   abft_stencil* lo_peer = nullptr;
@@ -571,7 +622,31 @@ void set_fwd(Group& G, const XSpec& x) {
   }
 }
 
+// IPC transport (one process per slab): the kernels stored the halos into
+// the neighbours' mapped buffers; order the next sweep of each slab after its
+// neighbours' sweep.  Exchange #s records this rank's event of parity s,
+// publishes s in its host-shared slot, waits until each neighbour published
+// s and enqueues a wait on the neighbour's event of parity s.  A neighbour
+// re-records that event only at exchange s + 2, which it reaches after this
+// rank published s + 1 -- i.e. after the wait below was enqueued.
+int sync_ipc(abft_stencil* h) {
+  on_dev(h);
+  const int64_t s = ++h->xseq;
+  CK(cudaEventRecord(h->ev_ipc[s & 1], h->stream));
+  __atomic_store_n(&h->shm[h->cfg.rank].seq, s, __ATOMIC_RELEASE);
+  for (abft_stencil* q : {h->lo_peer, h->hi_peer}) {
+    if (!q) continue;
+    while (__atomic_load_n(&h->shm[q->cfg.rank].seq, __ATOMIC_ACQUIRE) < s) sched_yield();
+    CK(cudaStreamWaitEvent(h->stream, q->ev_ipc[s & 1], 0));
+  }
+  return ABFT_OK;
+}
+
 int halo_exchange(Group& G, const XSpec& x) {
+  if (G.size() == 1 && G[0]->ipc) {
+    G[0]->fwd_buf = -1;
+    return sync_ipc(G[0]);
+  }
   if (G.size() > 1 && G[0]->fused) {
     for (abft_stencil* h : G) h->fwd_buf = -1;
     return sync_local(G);
@@ -655,11 +730,38 @@ int none_sweep(Group& G) {
   return ABFT_OK;
 }
 
+// IPC transport: the window verdict (dirty, extent) is max-reduced over every
+// rank through the host-shared slots.  Window w's values go to parity w & 1
+// once every rank has reduced window w - 2 (nobody still reads that parity).
+int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
+  on_dev(h);
+  int d[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(d, &h->st->dirty, sizeof(d), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const int64_t w = ++h->wseq;
+  const int n = h->cfg.nranks, me = h->cfg.rank, par = (int)(w & 1);
+  for (int r = 0; r < n; ++r)
+    while (__atomic_load_n(&h->shm[r].wdone, __ATOMIC_ACQUIRE) < w - 2) sched_yield();
+  for (int k = 0; k < 3; ++k) h->shm[me].val[par][k] = d[k];
+  __atomic_store_n(&h->shm[me].wseq, w, __ATOMIC_RELEASE);
+  int m[3] = {0, 0, 0};
+  for (int r = 0; r < n; ++r) {
+    while (__atomic_load_n(&h->shm[r].wseq, __ATOMIC_ACQUIRE) < w) sched_yield();
+    for (int k = 0; k < 3; ++k) m[k] = std::max(m[k], h->shm[r].val[par][k]);
+  }
+  __atomic_store_n(&h->shm[me].wdone, w, __ATOMIC_RELEASE);
+  *dirty = m[0];
+  *zmin = 0x7fffffffLL - m[1];
+  *zmax = (int64_t)m[2] - 1;
+  return ABFT_OK;
+}
+
 // the last window check over every slab of the job: flagged layers (> 0:
 // dirty) and the global extent [zmin, zmax] of the flagged layers
 int read_dirty(Group& G, int* dirty, int64_t* zmin, int64_t* zmax) {
   *dirty = 0;
   int ext[2] = {0, 0};
+  if (G.size() == 1 && G[0]->ipc) return read_dirty_ipc(G[0], dirty, zmin, zmax);
   for (abft_stencil* h : G) {
     on_dev(h);
     if (G.size() == 1 && h->cfg.nranks > 1) {
@@ -845,6 +947,80 @@ int step_group(Group& G, int32_t n) {
   }
   for (int i = 0; i < n; ++i) TRY(mode == ABFT_MODE_ONLINE ? online_sweep(G) : none_sweep(G));
   return ABFT_OK;
+}
+
+// ---------------------------------------------------------------- IPC
+// What a rank shares with its neighbours (abft_stencil_ipc_export): IPC
+// handles of its field buffers and aux workspace (each with the offset of the
+// handle's buffer in its allocation), the aux layout, and its two IPC events.
+struct IpcBlob {
+  uint32_t magic, version;
+  int32_t rank, nranks, nbuf, pad;
+  int64_t nx, ny, z_count, z_begin, plane, esz;
+  cudaIpcMemHandle_t mem[4];   // field buffers 0..2, aux
+  uint64_t off[4];
+  uint64_t off_gA[3], off_gB[3], off_PA[2], off_PB[2];
+  cudaIpcEventHandle_t ev[2];
+};
+static_assert(sizeof(IpcBlob) <= ABFT_IPC_BLOB_BYTES, "blob size");
+constexpr uint32_t kIpcMagic = 0xAB5F1C01u;
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<AddrRangeFn>(p);
+  }
+  return fn;
+}
+
+// the allocation containing ptr: IPC handle + offset of ptr in it
+int ipc_handle(const void* ptr, cudaIpcMemHandle_t* hd, uint64_t* off) {
+  AddrRangeFn fn = addr_range_fn();
+  if (!fn) return ABFT_ECUDA;
+  CUdeviceptr base = 0;
+  size_t sz = 0;
+  if (fn(&base, &sz, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return ABFT_ECUDA;
+  CK(cudaIpcGetMemHandle(hd, reinterpret_cast<void*>(base)));
+  *off = reinterpret_cast<uintptr_t>(ptr) - base;
+  return ABFT_OK;
+}
+
+// map a neighbour's allocation once per process (an allocation may hold
+// several of its buffers)
+int ipc_open(abft_stencil* h, std::vector<std::pair<cudaIpcMemHandle_t, char*>>& seen,
+             const cudaIpcMemHandle_t& hd, char** base) {
+  for (auto& e : seen)
+    if (!memcmp(&e.first, &hd, sizeof(hd))) { *base = e.second; return ABFT_OK; }
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  h->ipc_opened.push_back(p);
+  seen.push_back({hd, static_cast<char*>(p)});
+  *base = static_cast<char*>(p);
+  return ABFT_OK;
+}
+
+void ipc_unlink(abft_stencil* h) {
+  for (int f = 0; f < 2; ++f) {
+    abft_stencil* q = h->proxy[f];
+    if (!q) continue;
+    for (auto e : q->ev_ipc)
+      if (e) cudaEventDestroy(e);
+    delete q;
+    h->proxy[f] = nullptr;
+  }
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
+  for (auto e : h->ev_ipc)
+    if (e) cudaEventDestroy(e);
+  h->ev_ipc[0] = h->ev_ipc[1] = nullptr;
+  if (h->ipc) { h->lo_peer = h->hi_peer = nullptr; h->ipc = false; h->fused = false; }
 }
 
 }  // namespace
@@ -1082,13 +1258,10 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   // multi-GPU: NCCL communicator over NVLink, initial halo.  Without an id the
   // handle is a member of a local group (abft_stencil_group links them).
   if (cfg->nranks > 1 && cfg->nccl_unique_id) {
-    NcclApi* n = nccl_api();
-    if (!n) return fail(ABFT_ENCCL);
-    ncclUniqueId id;
-    memcpy(&id, cfg->nccl_unique_id, sizeof(id));
-    if (n->commInitRank(&h->comm, cfg->nranks, id, cfg->rank) != ncclSuccess) return fail(ABFT_ENCCL);
-    int r = exchange_nccl(h, XSpec{0, XV_GEN, 0});
-    if (r) { n->commDestroy(h->comm); return fail(r); }
+    int r = comm_acquire(cfg->nccl_unique_id, cfg->nranks, cfg->rank, &h->comm);
+    if (r) return fail(r);
+    r = exchange_nccl(h, XSpec{0, XV_GEN, 0});
+    if (r) { comm_release(h->comm); return fail(r); }
   }
   *out = h;
   return ABFT_OK;
@@ -1124,7 +1297,7 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
   if (!hs || n < 2) return ABFT_EINVAL;
   for (int i = 0; i < n; ++i) {
     abft_stencil* h = hs[i];
-    if (!h || h->grouped || h->comm || h->cfg.nranks != n || h->cfg.rank != i) return ABFT_EINVAL;
+    if (!h || h->grouped || h->comm || h->ipc || h->cfg.nranks != n || h->cfg.rank != i) return ABFT_EINVAL;
     const abft_config &a = h->cfg, &b = hs[0]->cfg;
     if (!same_problem(a, b)) return ABFT_EINVAL;
     if (i + 1 < n && a.z_begin + a.z_count != hs[i + 1]->cfg.z_begin) return ABFT_EINVAL;
@@ -1165,6 +1338,109 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
     CK(cudaEventCreateWithFlags(&h->ev_pulled, cudaEventDisableTiming));
   }
   return exchange_local(G, XSpec{0, XV_GEN, 0});  // initial halo of u^0 and a^0, b^0
+}
+
+int abft_stencil_ipc_export(abft_stencil* h, void* blob) {
+  if (!h || !blob || h->is_proxy || h->grouped || h->comm || h->cfg.nranks < 2) return ABFT_EINVAL;
+  DevScope ds(h);
+  IpcBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kIpcMagic;
+  b.version = 1;
+  b.rank = h->cfg.rank; b.nranks = h->cfg.nranks; b.nbuf = h->nbuf;
+  b.nx = h->cfg.nx; b.ny = h->cfg.ny; b.z_count = h->cfg.z_count; b.z_begin = h->cfg.z_begin;
+  b.plane = h->L.plane; b.esz = h->L.esz;
+  for (int k = 0; k < h->nbuf; ++k) TRY(ipc_handle(h->fb[k], &b.mem[k], &b.off[k]));
+  TRY(ipc_handle(h->aux, &b.mem[3], &b.off[3]));
+  for (int g = 0; g < 3; ++g) { b.off_gA[g] = h->L.off_gA[g]; b.off_gB[g] = h->L.off_gB[g]; }
+  for (int g = 0; g < 2; ++g) { b.off_PA[g] = h->L.off_PA[g]; b.off_PB[g] = h->L.off_PB[g]; }
+  for (int k = 0; k < 2; ++k) {
+    if (!h->ev_ipc[k]) CK(cudaEventCreateWithFlags(&h->ev_ipc[k], cudaEventDisableTiming | cudaEventInterprocess));
+    CK(cudaIpcGetEventHandle(&b.ev[k], h->ev_ipc[k]));
+  }
+  // a neighbour reads this slab's initial state as soon as it has the blob
+  CK(cudaStreamSynchronize(h->stream));
+  memset(blob, 0, ABFT_IPC_BLOB_BYTES);
+  memcpy(blob, &b, sizeof(b));
+  return ABFT_OK;
+}
+
+int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_blob, void* shm) {
+  if (!h || !shm || h->is_proxy || h->grouped || h->comm || h->ipc || h->cfg.nranks < 2 || h->sweeps != 0)
+    return ABFT_EINVAL;
+  if ((h->has_lo != 0) != (lo_blob != nullptr) || (h->has_hi != 0) != (hi_blob != nullptr)) return ABFT_EINVAL;
+  if (!h->ev_ipc[0]) return ABFT_EINVAL;   // export first (it creates the events the neighbours open)
+  DevScope ds(h);
+  const void* blobs[2] = {lo_blob, hi_blob};
+  std::vector<std::pair<cudaIpcMemHandle_t, char*>> seen;
+  int r = ABFT_OK;
+  for (int f = 0; f < 2 && r == ABFT_OK; ++f) {
+    if (!blobs[f]) continue;
+    IpcBlob b;
+    memcpy(&b, blobs[f], sizeof(b));
+    const int want = h->cfg.rank + (f == 0 ? -1 : 1);
+    const int64_t want_z = f == 0 ? h->cfg.z_begin - b.z_count : h->cfg.z_begin + h->cfg.z_count;
+    if (b.magic != kIpcMagic || b.version != 1 || b.rank != want || b.nranks != h->cfg.nranks ||
+        b.nx != h->cfg.nx || b.ny != h->cfg.ny || b.plane != h->L.plane || b.esz != h->L.esz ||
+        b.nbuf != h->nbuf || b.z_begin != want_z) {
+      r = ABFT_EINVAL;
+      break;
+    }
+    abft_stencil* q = new abft_stencil();
+    q->is_proxy = true;
+    q->cfg = h->cfg;
+    q->cfg.rank = b.rank;
+    q->cfg.z_begin = b.z_begin;
+    q->cfg.z_count = b.z_count;
+    q->L = h->L;
+    q->dev = h->dev;
+    h->proxy[f] = q;
+    for (int k = 0; k < b.nbuf && r == ABFT_OK; ++k) {
+      char* base = nullptr;
+      r = ipc_open(h, seen, b.mem[k], &base);
+      if (r == ABFT_OK) q->fb[k] = base + b.off[k];
+    }
+    char* base = nullptr;
+    if (r == ABFT_OK) r = ipc_open(h, seen, b.mem[3], &base);
+    if (r != ABFT_OK) break;
+    char* aux = base + b.off[3];
+    for (int g = 0; g < 3; ++g) {
+      q->gA[g] = reinterpret_cast<double*>(aux + b.off_gA[g]);
+      q->gB[g] = reinterpret_cast<double*>(aux + b.off_gB[g]);
+    }
+    for (int g = 0; g < 2; ++g) {
+      q->PA[g] = reinterpret_cast<double*>(aux + b.off_PA[g]);
+      q->PB[g] = reinterpret_cast<double*>(aux + b.off_PB[g]);
+    }
+    for (int k = 0; k < 2 && r == ABFT_OK; ++k)
+      if (cudaIpcOpenEventHandle(&q->ev_ipc[k], b.ev[k]) != cudaSuccess) r = ABFT_ECUDA;
+  }
+  if (r != ABFT_OK) {
+    ipc_unlink(h);
+    return r;
+  }
+  h->lo_peer = h->proxy[0];
+  h->hi_peer = h->proxy[1];
+  h->ipc = true;
+  h->fused = true;
+  h->shm = static_cast<abft_ipc_slot*>(shm);
+  h->xseq = h->wseq = 0;
+  memset(&h->shm[h->cfg.rank], 0, sizeof(abft_ipc_slot));
+  // initial halo of u^0 and a^0, b^0: pull the neighbours' boundary layers
+  // (their exports synchronised their init); their first writes into these
+  // buffers come after their first sweep, which waits for this rank's
+  const size_t lb = (size_t)h->L.plane * h->L.esz;
+  const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
+  for (int f = 0; f < 2; ++f) {
+    abft_stencil* q = h->proxy[f];
+    if (!q) continue;
+    const int64_t src_l = f == 0 ? q->cfg.z_count : 1, dst_l = f == 0 ? 0 : zc + 1;
+    CK(cudaMemcpyAsync(h->fb[0] + dst_l * lb, q->fb[0] + src_l * lb, lb, cudaMemcpyDefault, h->stream));
+    CK(cudaMemcpyAsync(h->gA[0] + dst_l * nx, q->gA[0] + src_l * nx, nx * 8, cudaMemcpyDefault, h->stream));
+    CK(cudaMemcpyAsync(h->gB[0] + dst_l * ny, q->gB[0] + src_l * ny, ny * 8, cudaMemcpyDefault, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return ABFT_OK;
 }
 
 int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps) {
@@ -1256,7 +1532,8 @@ int abft_stencil_set_faults(abft_stencil* h, const abft_fault* f, int32_t n) {
     h->faults.push_back(PendingFault{a, false});
   }
   // one K1 launch carries a sweep's flips in its parameter block: at most
-  // kMaxFaultsPerLaunch per sweep in this slab, one per cell
+  // kMaxFaultsPerLaunch per sweep in this slab (a cell listed k times for one
+  // sweep strikes k executions of it: the first and k - 1 re-executions)
   std::vector<const abft_fault*> mine;
   for (const PendingFault& pf : h->faults) {
     const int64_t zl = pf.f.z - h->cfg.z_begin;
@@ -1267,9 +1544,7 @@ int abft_stencil_set_faults(abft_stencil* h, const abft_fault* f, int32_t n) {
   });
   for (size_t i = 0, run = 1; i < mine.size(); ++i, ++run) {
     if (i > 0 && mine[i]->sweep != mine[i - 1]->sweep) run = 1;
-    const bool same_cell = i > 0 && mine[i]->sweep == mine[i - 1]->sweep && mine[i]->z == mine[i - 1]->z &&
-                           mine[i]->y == mine[i - 1]->y && mine[i]->x == mine[i - 1]->x;
-    if (same_cell || run > (size_t)kMaxFaultsPerLaunch) {
+    if (run > (size_t)kMaxFaultsPerLaunch) {
       h->faults.clear();
       return ABFT_EINVAL;
     }
@@ -1409,10 +1684,8 @@ int abft_stencil_destroy(abft_stencil* h) {
   for (abft_stencil* q : h->members)   // unlink: the group is unusable once a member is gone
     if (q != h) { q->lo_peer = q->lo_peer == h ? nullptr : q->lo_peer;
                   q->hi_peer = q->hi_peer == h ? nullptr : q->hi_peer; q->members.clear(); }
-  if (h->comm) {
-    NcclApi* n = nccl_api();
-    if (n) n->commDestroy(h->comm);
-  }
+  if (h->comm) comm_release(h->comm);
+  ipc_unlink(h);
   delete h;
   return ABFT_OK;
 }

@@ -12,6 +12,8 @@
 // cells of the column (Q11) and the checksums repaired exactly (Q12).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace abft {
@@ -571,10 +573,13 @@ struct ConstVal {   // C_{x,y} = sum_q coef_q * src_q (fp64, dtype-rounded opera
     return field ? static_cast<const char*>(field) + ((size_t)z * fplane + (size_t)y * fpx) * (dtype == ABFT_F32 ? 4 : 8)
                  : nullptr;
   }
-  // C from the field value at this cell (unused without a field source)
+  // C from the field value at this cell (unused without a field source);
+  // compile-time indices keep coef / scalar in the parameter bank
   __device__ __forceinline__ double val(double fv, int) const {
     double s = 0.0;
-    for (int q = 0; q < nsources; ++q) {
+#pragma unroll
+    for (int q = 0; q < kMaxSources; ++q) {
+      if (q >= nsources) break;
       const double t = __dmul_rn(coef[q], q == field_src ? fv : scalar[q]);
       s = (q == 0) ? t : __dadd_rn(s, t);
     }
@@ -588,24 +593,54 @@ __device__ __forceinline__ double k0_ld(const char* row, int dtype, int x) {
                            : __ldg(reinterpret_cast<const double*>(row) + x);
 }
 
-// A[z][x] = sum_y f(z, y, x); 1D grid of zc x ceil(nx / 256) CTAs; out row
-// stride nx, layer offset `off`
-template <typename F>
-__global__ void __launch_bounds__(256) k0_colsum(F f, int dtype, int nx, int ny, double* A, int off) {
-  const int64_t nxb = (nx + 255) / 256;
-  const int z = (int)(blockIdx.x / nxb), x = (int)(blockIdx.x % nxb) * 256 + threadIdx.x;
-  if (x >= nx) return;
-  double s = 0.0;
+// A[z][x] = sum_y f(z, y, x); 1D grid of zc x ceil(nx / (256 V)) CTAs, a
+// thread owns V consecutive columns (one 16-byte vector: V = 4 fp32, 2 fp64;
+// element loads on a ragged row end); out row stride nx, layer offset `off`
+template <typename F, typename T>
+__global__ void __launch_bounds__(256) k0_colsum(F f, int nx, int ny, double* A, int off) {
+  constexpr int V = 16 / (int)sizeof(T), U = 8;
+  using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const int64_t nxb = (nx + 256 * V - 1) / (256 * V);
+  const int z = (int)(blockIdx.x / nxb), x0 = ((int)(blockIdx.x % nxb) * 256 + threadIdx.x) * V;
+  if (x0 >= nx) return;
+  const bool whole = x0 + V <= nx;
+  double s[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) s[k] = 0.0;
+  auto load = [&](int y, T (&v)[V]) {
+    const char* row = f.row(z, y);
+    if (!row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = T(0);
+    } else if (whole) {
+      const VT w = __ldg(reinterpret_cast<const VT*>(reinterpret_cast<const T*>(row) + x0));
+      const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = e[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = x0 + k < nx ? __ldg(reinterpret_cast<const T*>(row) + x0 + k) : T(0);
+    }
+  };
   int y = 0;
-  for (; y + 8 <= ny; y += 8) {
-    double v[8];
+  for (; y + U <= ny; y += U) {
+    T v[U][V];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = k0_ld(f.row(z, y + j), dtype, x);
+    for (int j = 0; j < U; ++j) load(y + j, v[j]);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s = __dadd_rn(s, f.val(v[j], x));
+    for (int j = 0; j < U; ++j)
+#pragma unroll
+      for (int k = 0; k < V; ++k) s[k] = __dadd_rn(s[k], f.val((double)v[j][k], x0 + k));
   }
-  for (; y < ny; ++y) s = __dadd_rn(s, f.val(k0_ld(f.row(z, y), dtype, x), x));
-  A[(size_t)(z + off) * nx + x] = s;
+  for (; y < ny; ++y) {
+    T v[V];
+    load(y, v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) s[k] = __dadd_rn(s[k], f.val((double)v[k], x0 + k));
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k)
+    if (x0 + k < nx) A[(size_t)(z + off) * nx + x0 + k] = s[k];
 }
 
 // B[z][y] = sum_x f(z, y, x); one thread per row, 128-byte segments of the

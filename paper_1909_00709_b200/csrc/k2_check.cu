@@ -114,7 +114,10 @@ cudaError_t prime_checks(int dtype, int shape, int bc) {
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s) {
   FieldVal f{u, px, plane, dtype};
-  k0_colsum<<<(unsigned)((int64_t)zc * ((nx + 255) / 256)), 256, 0, s>>>(f, dtype, nx, ny, A, off);
+  const int V = dtype == ABFT_F32 ? 4 : 2;
+  const unsigned cb = (unsigned)((int64_t)zc * ((nx + 256 * V - 1) / (256 * V)));
+  if (dtype == ABFT_F32) k0_colsum<FieldVal, float><<<cb, 256, 0, s>>>(f, nx, ny, A, off);
+  else k0_colsum<FieldVal, double><<<cb, 256, 0, s>>>(f, nx, ny, A, off);
   k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, B, off);
   return cudaGetLastError();
 }
@@ -129,7 +132,10 @@ cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, i
     f.coef[q] = q < nsources ? coef[q] : 0.0;
     f.scalar[q] = q < nsources ? scalar[q] : 0.0;
   }
-  k0_colsum<<<(unsigned)((int64_t)zc * ((nx + 255) / 256)), 256, 0, s>>>(f, dtype, nx, ny, cA, 0);
+  const int V = dtype == ABFT_F32 ? 4 : 2;
+  const unsigned cb = (unsigned)((int64_t)zc * ((nx + 256 * V - 1) / (256 * V)));
+  if (dtype == ABFT_F32) k0_colsum<ConstVal, float><<<cb, 256, 0, s>>>(f, nx, ny, cA, 0);
+  else k0_colsum<ConstVal, double><<<cb, 256, 0, s>>>(f, nx, ny, cA, 0);
   k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, cB, 0);
   return cudaGetLastError();
 }

@@ -40,7 +40,8 @@ def test_library_exports_every_declared_symbol(L):
 def test_struct_sizes_match_header_layout(tmp_path):
     # the ctypes mirrors against the header itself, compiled with gcc
     src = tmp_path / "sz.c"
-    names = ["abft_point", "abft_source", "abft_fault", "abft_record", "abft_stats", "abft_config"]
+    names = ["abft_point", "abft_source", "abft_fault", "abft_record", "abft_stats", "abft_config",
+             "abft_ipc_slot"]
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "abft_stencil.h"\nint main(void){'
                    + "".join(f'printf("%zu\\n", sizeof({n}));' for n in names)
                    + 'printf("%zu\\n", offsetof(abft_config, recovery));return 0;}\n')

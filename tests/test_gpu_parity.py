@@ -330,13 +330,14 @@ def test_lazy_slab_group_equals_oracle(G, halo):
     assert np.array_equal(g["A"], o["A"]) and np.array_equal(g["B"], o["B"])
 
 
-def test_set_faults_rejects_duplicates_and_overfull_sweeps():
+def test_set_faults_rejects_overfull_sweeps():
     from paper_1909_00709_b200 import abft
     p = make_problem("cfg2", nx=64, ny=64, nz=80, sweeps=2)
     dev = torch.device("cuda:0")
     st = abft.from_problem(p, field_u0(p, dev), field_power(p, dev), device=dev)
+    st.set_faults([Fault(1, 3, 4, 5, 20), Fault(1, 3, 4, 5, 21)])   # a repeat strikes a re-execution
     with pytest.raises(abft.AbftError):
-        st.set_faults([Fault(1, 3, 4, 5, 20), Fault(1, 3, 4, 5, 21)])
+        st.set_faults([Fault(1, 3, 4, 5, 20)] * 65)
     with pytest.raises(abft.AbftError):
         st.set_faults([Fault(1, z, 0, 0, 20) for z in range(65)])
     st.set_faults([Fault(1, z, 0, 0, 20) for z in range(64)] + [Fault(2, 0, 0, 0, 20)])
@@ -542,8 +543,11 @@ def test_offline_partial_keeps_undetected_error_outside_the_cone():
     assert np.array_equal(g["u"].view(np.uint32), only_lo["u"].view(np.uint32))
 
 
-def test_offline_partial_persistent_error():
-    p = make_problem("cfg3", nx=32, ny=32, nz=10, sweeps=10, mode=2, delta=5, recovery=1)
+@pytest.mark.parametrize("recovery", [0, 1])
+def test_offline_persistent_error(recovery):
+    # the same flip listed twice strikes the window's execution and its
+    # re-execution: the re-check still flags, PERSISTENT records
+    p = make_problem("cfg3", nx=32, ny=32, nz=10, sweeps=10, mode=2, delta=5, recovery=recovery)
     g, o = parity(p, faults=[Fault(3, 1, 5, 5, 30), Fault(3, 1, 5, 5, 30)])
     assert o["status"] == 3 and o["stats"]["persistent"] == 1
 
