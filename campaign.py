@@ -17,6 +17,11 @@ E2 (fig.biterror): 64x64x8, 128 iterations, for every bit position
    correction, offline rollback erases every detected flip.
 E3 (fig.interval): offline detection period 1..128 on both tiles,
    error-free and with one flip: mean time per run.
+Offline runs come twice: with the full rollback of a dirty window (the
+paper's, P:742) and with the partial re-execution of the flagged layers'
+light cone (recovery PARTIAL, "exploit stencil locality to reduce the
+re-execution cost"; Q28) -- the 512x512x64 tile (cfg3's)
+shows what the locality saves when the layers outnumber the cone.
 
 Every run is seeded (abft_inputs); the l2 norm is computed on the device in
 fp64.  Prints one JSON object per experiment and writes them to --out.
@@ -40,13 +45,16 @@ import torch  # noqa: E402
 from abft_inputs import Fault, field_power, field_u0, make_problem  # noqa: E402
 
 TILES = {"64x64x8": dict(nx=64, ny=64, nz=8, sweeps=128),
-         "512x512x8": dict(nx=512, ny=512, nz=8, sweeps=256)}
-MODES = {"none": 0, "online": 1, "offline": 2}
+         "512x512x8": dict(nx=512, ny=512, nz=8, sweeps=256),
+         "512x512x64": dict(nx=512, ny=512, nz=64, sweeps=128)}
+MODES = {"none": 0, "online": 1, "offline": 2, "offline_partial": 2}
 
 
 def problem(tile: str, mode: str, **kw):
-    """HotSpot3D-like tile of BASELINE.json configs[1] at the paper's sizes (Table 1)."""
-    return make_problem("cfg2", **TILES[tile], mode=MODES[mode], delta=kw.pop("delta", 16), **kw)
+    """HotSpot3D-like tile of BASELINE.json configs[1] at the paper's sizes (Table 1,
+    P:793; 512x512x64 = configs[2]).  offline_partial: recovery PARTIAL (Q28)."""
+    return make_problem("cfg2", **TILES[tile], mode=MODES[mode], delta=kw.pop("delta", 16),
+                        recovery=1 if mode == "offline_partial" else 0, **kw)
 
 
 class Runner:
@@ -133,7 +141,7 @@ def exp_e1(R: Runner, reps: int, seed: int = 1, policy: int = 0):
                 "rollbacks": sum(r["stats"]["rollbacks"] for r in faulty),
             }
         base = res["none"]["ms_error_free"]
-        for mode in ("online", "offline"):
+        for mode in ("online", "offline", "offline_partial"):
             res[mode]["overhead_error_free_pct"] = 100.0 * (res[mode]["ms_error_free"] / base - 1.0)
         out["tiles"][tile] = dict(sweeps=TILES[tile]["sweeps"], reps=reps, modes=res)
     return out
@@ -173,8 +181,10 @@ def exp_e3(R: Runner, reps: int, seed: int = 3, policy: int = 0,
             p = problem(tile, "offline", delta=d)
             clean = statistics.median(R.run(p)["ms"] for _ in range(3))
             faulty = [R.run(p, [f]) for f in flips]
+            part = [R.run(problem(tile, "offline_partial", delta=d), [f]) for f in flips]
             rows[d] = {"ms_error_free": clean, "overhead_error_free_pct": 100.0 * (clean / base - 1.0),
                        "ms_one_flip_mean": statistics.fmean(r["ms"] for r in faulty),
+                       "ms_one_flip_mean_partial": statistics.fmean(r["ms"] for r in part),
                        "rollbacks_mean": statistics.fmean(r["stats"]["rollbacks"] for r in faulty)}
         out["tiles"][tile] = dict(no_abft_ms=base, periods=rows)
     return out

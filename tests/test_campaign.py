@@ -12,7 +12,7 @@ from tests.parity_util import assert_records_equal, oracle_run
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["none", "online", "offline"])
+@pytest.mark.parametrize("mode", ["none", "online", "offline", "offline_partial"])
 def test_campaign_trials_equal_oracle(mode):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")

@@ -114,7 +114,10 @@ def _bits(t):
 
 
 def _need_memory(p):
+    import gc
     import psutil
+    gc.collect()
+    torch.cuda.empty_cache()      # blocks the earlier tests left in torch's cache
     free, total = torch.cuda.mem_get_info()
     need_dev = 4 * p.cells * 8                 # 3 field buffers + the initial slab
     need_host = 2 * p.cells * 8 + (16 << 30)   # two final fields + headroom

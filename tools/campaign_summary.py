@@ -45,5 +45,8 @@ if "E3" in by:
     for t, v in e3["tiles"].items():
         print(f"| {t} error-free | {v['no_abft_ms']:.3f} | " + " | ".join(f"{x['ms_error_free']:.3f}" for x in v["periods"].values()) + " |")
         print(f"| {t} one flip | | " + " | ".join(f"{x['ms_one_flip_mean']:.3f}" for x in v["periods"].values()) + " |")
+        if all("ms_one_flip_mean_partial" in x for x in v["periods"].values()):
+            print(f"| {t} one flip, partial re-execution | | " +
+                  " | ".join(f"{x['ms_one_flip_mean_partial']:.3f}" for x in v["periods"].values()) + " |")
     print("\nAs in P:944-951 the per-window cost (one host synchronisation for the verdict; the checkpoint is a "
           "buffer rotation, no copy) amortises with the period; with a flip, long periods re-execute more.")
