@@ -130,8 +130,8 @@ typedef struct {
   int64_t z_begin;      /* first global layer of this rank's slab */
   int64_t z_count;      /* layers owned by this rank, >= 1 */
   int32_t dtype;        /* abft_dtype */
-  int32_t bc;           /* abft_bc: all four; PERIODIC needs nranks == 1 (else
-                           ABFT_EUNSUPPORTED) and always runs the z-march K1 */
+  int32_t bc;           /* abft_bc: all four; PERIODIC over several ranks closes
+                           the z ring (rank 0 and the last rank are neighbours) */
   double bc_value;      /* ghost value for ABFT_BC_CONSTANT */
   int32_t npoints;      /* 1 .. 27 */
   int32_t nsources;     /* 0 .. 4 */
@@ -243,7 +243,7 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n);
 /* The z-slab halo plan of cfg (one process per GPU, NCCL): for the lower
  * (plan[0..2]) and upper (plan[3..5]) face, the peer rank, the buffer layer
  * sent (1 or z_count) and the halo layer received (0 or z_count + 1); -1
- * where there is no neighbour.  No device needed. */
+ * where there is no neighbour (a periodic ring has none).  No device needed. */
 int abft_stencil_halo_plan(const abft_config* cfg, int32_t plan[6]);
 int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps);
 
@@ -261,7 +261,8 @@ int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps)
  *   3. abft_stencil_ipc_link(h, lo_blob, hi_blob, shm): maps the neighbours'
  *      buffers (peer access over NVLink, or the same GPU), opens their events,
  *      pulls the initial halo and zeroes this rank's progress slot.  lo_blob /
- *      hi_blob: the blob of rank - 1 / rank + 1, NULL at a global face.  shm:
+ *      hi_blob: the blob of rank - 1 / rank + 1 (modulo nranks for a periodic
+ *      ring), NULL at a global face.  shm:
  *      an array of nranks abft_ipc_slot in host memory mapped by every
  *      process of the job (e.g. a /dev/shm segment), zero-initialised; the
  *      caller keeps it mapped until destroy.  Every rank must have linked (a

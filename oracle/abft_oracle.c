@@ -533,6 +533,9 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
             const int64_t r = 2 * (wend - s - 1);
             zlo = zmin - r < 0 ? 0 : zmin - r;
             zhi = zmax + r > nz - 1 ? nz - 1 : zmax + r;
+            /* periodic z: a reach past a face wraps to the far layers -- take
+               every layer then */
+            if (p->bc == OR_BC_PERIODIC && (zmin - r < 0 || zmax + r > nz - 1)) { zlo = 0; zhi = nz - 1; }
             memcpy(first, cur, fb);
           }
           if (cur != ckpt) memcpy(cur, ckpt, fb);

@@ -196,9 +196,6 @@ int validate(const abft_config* c) {
     return ABFT_EINVAL;
   }
   if (c->bc == ABFT_BC_CONSTANT && !isfinite(c->bc_value)) return ABFT_EINVAL;
-  // periodic wraps z across the whole domain: one slab only (a ring exchange
-  // between the first and last rank is not implemented)
-  if (c->bc == ABFT_BC_PERIODIC && c->nranks > 1) return ABFT_EUNSUPPORTED;
   return ABFT_OK;
 }
 
@@ -528,10 +525,13 @@ void xvecs(abft_stencil* h, const XSpec& x, double** a, double** b) {
 // 1 = upper) the peer rank, the buffer layer sent and the halo layer received
 // (-1 when there is no neighbour) -- the plan paper_1909_00709_b200/dist.py
 // states and tests with gloo
+// Periodic z over several ranks closes the ring: rank 0's lower neighbour is
+// the last rank and vice versa.
+bool z_ring(const abft_config& c) { return c.bc == ABFT_BC_PERIODIC && c.nranks > 1; }
 void halo_plan(const abft_config& c, int32_t plan[6]) {
   for (int side = 0; side < 2; ++side) {
-    const bool has = side == 0 ? c.rank > 0 : c.rank < c.nranks - 1;
-    plan[3 * side + 0] = has ? c.rank + (side == 0 ? -1 : 1) : -1;
+    const bool has = z_ring(c) || (side == 0 ? c.rank > 0 : c.rank < c.nranks - 1);
+    plan[3 * side + 0] = has ? (c.rank + (side == 0 ? -1 : 1) + c.nranks) % c.nranks : -1;
     plan[3 * side + 1] = has ? (side == 0 ? 1 : (int32_t)c.z_count) : -1;
     plan[3 * side + 2] = has ? (side == 0 ? 0 : (int32_t)c.z_count + 1) : -1;
   }
@@ -549,7 +549,12 @@ int exchange_nccl(abft_stencil* h, const XSpec& x) {
   int32_t plan[6];
   halo_plan(h->cfg, plan);
   if (n->groupStart() != ncclSuccess) return ABFT_ENCCL;
-  for (int side = 0; side < 2; ++side) {
+  // sends / receives to one peer are matched in posting order: with a ring of
+  // two ranks both faces face the same peer, so rank 1 posts its upper face
+  // first (rank 0's lower-face send lands in rank 1's upper halo)
+  const bool swap = z_ring(h->cfg) && h->cfg.nranks == 2 && h->cfg.rank == 1;
+  for (int k = 0; k < 2; ++k) {
+    const int side = swap ? 1 - k : k;
     const int peer = plan[3 * side];
     if (peer < 0) continue;
     const int64_t send_l = plan[3 * side + 1], recv_l = plan[3 * side + 2];
@@ -895,8 +900,14 @@ int offline_window(Group& G, int L) {
     if (attempt == 0) {
       // re-execution range of a partial recovery: every layer an error of
       // this window that was flagged can have reached (Q28)
+      const int64_t nzg = h0->cfg.nz_global;
       zlo = std::max<int64_t>(0, zmin - 2 * (L - 1));
-      zhi = std::min<int64_t>(h0->cfg.nz_global - 1, zmax + 2 * (L - 1));
+      zhi = std::min<int64_t>(nzg - 1, zmax + 2 * (L - 1));
+      // periodic z: a reach past a face wraps to the far layers -- take them all
+      if (h0->cfg.bc == ABFT_BC_PERIODIC && (zmin - 2 * (L - 1) < 0 || zmax + 2 * (L - 1) > nzg - 1)) {
+        zlo = 0;
+        zhi = nzg - 1;
+      }
     }
     for (abft_stencil* h : G) {
       if (attempt == 0) {
@@ -1007,6 +1018,7 @@ int ipc_open(abft_stencil* h, std::vector<std::pair<cudaIpcMemHandle_t, char*>>&
 }
 
 void ipc_unlink(abft_stencil* h) {
+  if (h->proxy[1] == h->proxy[0]) h->proxy[1] = nullptr;
   for (int f = 0; f < 2; ++f) {
     abft_stencil* q = h->proxy[f];
     if (!q) continue;
@@ -1096,8 +1108,8 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->lazy_mark = h->lazy_rowlist + 2 * (cfg->z_count + 2);
   for (int b = 0; b < 3; ++b) h->EX[b] = h->aux + L.off_EX[b];
   h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
-  h->has_lo = cfg->rank > 0;
-  h->has_hi = cfg->rank < cfg->nranks - 1;
+  h->has_lo = z_ring(*cfg) || cfg->rank > 0;
+  h->has_hi = z_ring(*cfg) || cfg->rank < cfg->nranks - 1;
   const int64_t nx = cfg->nx, ny = cfg->ny, zc = cfg->z_count;
   const int esz = L.esz;
   auto fail = [&](int code) { delete h; return code; };
@@ -1328,8 +1340,9 @@ int abft_stencil_group(abft_stencil* const* hs, int32_t n) {
   CK(cudaSetDevice(cur_dev));
   for (int i = 0; i < n; ++i) {
     abft_stencil* h = hs[i];
-    h->lo_peer = i > 0 ? hs[i - 1] : nullptr;
-    h->hi_peer = i + 1 < n ? hs[i + 1] : nullptr;
+    const bool ring = z_ring(h->cfg);
+    h->lo_peer = i > 0 ? hs[i - 1] : (ring ? hs[n - 1] : nullptr);
+    h->hi_peer = i + 1 < n ? hs[i + 1] : (ring ? hs[0] : nullptr);
     h->grouped = true;
     h->fused = fused;
     h->members = G;
@@ -1378,8 +1391,13 @@ int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_b
     if (!blobs[f]) continue;
     IpcBlob b;
     memcpy(&b, blobs[f], sizeof(b));
-    const int want = h->cfg.rank + (f == 0 ? -1 : 1);
-    const int64_t want_z = f == 0 ? h->cfg.z_begin - b.z_count : h->cfg.z_begin + h->cfg.z_count;
+    const int64_t nzg = h->cfg.nz_global;
+    const int want = (h->cfg.rank + (f == 0 ? -1 : 1) + h->cfg.nranks) % h->cfg.nranks;
+    const int64_t want_z = ((f == 0 ? h->cfg.z_begin - b.z_count : h->cfg.z_begin + h->cfg.z_count) + nzg) % nzg;
+    if (f == 1 && h->proxy[0] && lo_blob && !memcmp(lo_blob, hi_blob, sizeof(IpcBlob))) {
+      h->proxy[1] = h->proxy[0];   // a ring of two ranks: one neighbour on both faces
+      continue;
+    }
     if (b.magic != kIpcMagic || b.version != 1 || b.rank != want || b.nranks != h->cfg.nranks ||
         b.nx != h->cfg.nx || b.ny != h->cfg.ny || b.plane != h->L.plane || b.esz != h->L.esz ||
         b.nbuf != h->nbuf || b.z_begin != want_z) {

@@ -28,8 +28,9 @@ static cudaError_t k2_go(int shape, dim3 g, cudaStream_t s, const CheckParams& p
 
 cudaError_t launch_k2(int dtype, int shape, cudaStream_t s, const CheckParams& p) {
   const int zc = p.zr1 - p.zr0;   // layers of this launch
-  // one CTA per layer; few layers (cfg1-3 tiles): split each layer's entries
-  // over up to 2 x SMs / zc CTAs, at least kCheckThreads entries each
+  // one CTA per layer; few layers (< 2 per SM: cfg1-3 tiles, the cfg5 slab):
+  // split each layer's entries over up to ~8 x SMs / zc CTAs (the check is
+  // latency-bound: fill the GPU), at least kCheckThreads entries each
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -38,7 +39,7 @@ cudaError_t launch_k2(int dtype, int shape, cudaStream_t s, const CheckParams& p
   }
   int parts = 1;
   if (!(p.flags & CK_FROM_SUMMARY)) {
-    const int want = (2 * nsm + zc - 1) / zc;
+    const int want = zc >= 2 * nsm ? 1 : (8 * nsm + zc - 1) / zc;
     const int cap = (std::max(p.nx, p.ny) + kCheckThreads - 1) / kCheckThreads;
     parts = std::max(1, std::min(want, cap));
   }

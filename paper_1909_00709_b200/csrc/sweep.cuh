@@ -747,7 +747,10 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       __syncthreads();  // lowest staged layer consumed; this layer's column partials complete
       if (tid == 0) {
         fence_proxy_async();
-        if (it + NS < nT) issue_T(it + NS);
+        // the slot this layer freed: the lowest of its three planes, or
+        // (plane streaming) the one plane it read, two layers further on
+        const int fr = STREAM ? it + 2 : it;
+        if (fr + NS < nT) issue_T(fr + NS);
       }
     }
     if constexpr (CHK == K1_CK_AB) {
@@ -861,6 +864,12 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
     rotate();
     splane(1, true, false, true, zs + 1 < ze);
     rotate();
+    __syncthreads();   // planes zs - 1 and zs are consumed: refill their slots
+    if (tid == 0) {
+      fence_proxy_async();
+      for (int i = 0; i < 2; ++i)
+        if (i + NS < nT) issue_T(i + NS);
+    }
 #pragma unroll 1
     for (int z = zs; z < ze; ++z) {
       T pv[RY][V];

@@ -30,18 +30,21 @@ def weak_nz(nz_per_rank: int, world: int) -> int:
     return nz_per_rank * world
 
 
-def neighbours(rank: int, world: int) -> Tuple[Optional[int], Optional[int]]:
-    """(lower, upper) neighbour rank in z, None at a global face."""
+def neighbours(rank: int, world: int, periodic: bool = False) -> Tuple[Optional[int], Optional[int]]:
+    """(lower, upper) neighbour rank in z, None at a global face; a periodic
+    domain over several ranks closes the ring."""
+    if periodic and world > 1:
+        return ((rank - 1) % world, (rank + 1) % world)
     return (rank - 1 if rank > 0 else None, rank + 1 if rank + 1 < world else None)
 
 
-def halo_plan(rank: int, world: int, zc: int) -> List[Tuple[int, int, int]]:
+def halo_plan(rank: int, world: int, zc: int, periodic: bool = False) -> List[Tuple[int, int, int]]:
     """(peer, send_layer, recv_layer) per face, in buffer layers: the boundary
     layer goes to the neighbour, whose boundary layer lands in the halo slot.
     The checksum rows a[layer], b[layer] (or the offline prediction rows) of the
     same layers travel with them.  Lower face first -- the order the library
     posts its sends / receives inside one NCCL group."""
-    lo, hi = neighbours(rank, world)
+    lo, hi = neighbours(rank, world, periodic)
     plan = []
     if lo is not None:
         plan.append((lo, 1, 0))

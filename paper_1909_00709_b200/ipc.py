@@ -45,8 +45,10 @@ class IpcContext:
         blob = abft.ipc_export(st)
         blobs = [None] * self.world
         dist.all_gather_object(blobs, blob)
-        lo = blobs[self.rank - 1] if self.rank > 0 else None
-        hi = blobs[self.rank + 1] if self.rank + 1 < self.world else None
+        from .dist import neighbours
+        lo_r, hi_r = neighbours(self.rank, self.world, periodic=st.cfg.bc == abft.ABFT_BC_PERIODIC)
+        lo = blobs[lo_r] if lo_r is not None else None
+        hi = blobs[hi_r] if hi_r is not None else None
         abft.ipc_link(st, lo, hi, self.addr)
         dist.barrier()
 

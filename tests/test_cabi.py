@@ -89,8 +89,6 @@ def test_workspace_size_sane(L):
     (dict(points=[(0, 0, 0, float("inf"))]), abft.ABFT_EINVAL),
     (dict(mode=2, delta=0), abft.ABFT_EINVAL),
     (dict(mode=7), abft.ABFT_EINVAL),
-    (dict(bc=abft.ABFT_BC_PERIODIC, nranks=2, rank=0, z_count=2, nccl_unique_id=b"\0" * 128),
-     abft.ABFT_EUNSUPPORTED),                                  # periodic wrap across ranks
     (dict(bc=abft.ABFT_BC_CONSTANT, bc_value=float("inf")), abft.ABFT_EINVAL),
     (dict(bc=9), abft.ABFT_EINVAL),
     (dict(checksum_policy=2), abft.ABFT_EINVAL),
@@ -119,16 +117,22 @@ def test_multi_rank_slab_config_accepted(L):
     assert fb >= 64 * 32 * 4 * 4
 
 
+@pytest.mark.parametrize("periodic", [False, True])
 @pytest.mark.parametrize("nz,world", [(4, 1), (4, 2), (7, 3), (9, 4), (16, 8)])
-def test_library_halo_plan_matches_dist(L, nz, world):
+def test_library_halo_plan_matches_dist(L, nz, world, periodic):
     """The library's NCCL exchange plan (abft_stencil_halo_plan, used by
-    exchange_nccl) equals the host plan dist.halo_plan that the gloo tests run."""
+    exchange_nccl) equals the host plan dist.halo_plan that the gloo tests run;
+    a periodic domain over several ranks closes the ring."""
     from paper_1909_00709_b200 import dist
     for rank in range(world):
         z0, zc = dist.slab(nz, world, rank)
         c, keep = _cfg(nz=nz, nranks=world, rank=rank, z_begin=z0, z_count=zc,
-                       nccl_unique_id=b"\0" * 128 if world > 1 else None)
-        assert abft.abft_stencil_halo_plan(c) == dist.halo_plan(rank, world, zc)
+                       nccl_unique_id=b"\0" * 128 if world > 1 else None,
+                       bc=abft.ABFT_BC_PERIODIC if periodic else abft.ABFT_BC_CLAMP)
+        plan = dist.halo_plan(rank, world, zc, periodic)
+        assert abft.abft_stencil_halo_plan(c) == plan
+        if periodic and world > 1:
+            assert [p for p, _, _ in plan] == [(rank - 1) % world, (rank + 1) % world]
 
 
 def test_stencil_refuses_cpu_device(L):

@@ -401,14 +401,19 @@ def test_bc_slab_group(bc, halo):
     assert_records_equal(g, o)
 
 
-def test_bc_periodic_multi_rank_unsupported():
-    from paper_1909_00709_b200 import abft
-    p = make_problem("cfg3", nx=64, ny=64, nz=8, bc=1)
-    dev = torch.device("cuda:0")
-    with pytest.raises(abft.AbftError) as e:
-        abft.from_problem(p, field_u0(p, dev)[:4].contiguous(), field_power(p, dev)[:4].contiguous(),
-                          device=dev, z_begin=0, z_count=4, rank=0, nranks=2)
-    assert e.value.status == abft.ABFT_EUNSUPPORTED
+@pytest.mark.parametrize("G,mode", [(2, 1), (3, 1), (2, 2), (3, 2)])
+def test_bc_periodic_ring_of_slabs(G, mode, halo):
+    # periodic z over several slabs closes the ring: slab 0 and the last slab
+    # exchange halos (a ring of two: one neighbour on both faces)
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=mode, delta=5, bc=1)
+    faults = fault_schedule(p) + [Fault(9, 0, 3, 4, 30), Fault(9, 11, 70, 90, 29)]
+    faults = list({(f.sweep, f.z, f.y, f.x): f for f in faults}.values())
+    o = oracle_run(p, faults=faults)
+    g = _group_run(p, G, faults)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+    assert np.array_equal(g["A"], o["A"]) and np.array_equal(g["B"], o["B"])
 
 
 # ---- correction_form 2: recompute the located cell (stencil locality)

@@ -89,6 +89,9 @@ CASES = {
     "lazy": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=1, checksums=1),
     "offline": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=28, nfaults=8, mode=2, delta=7),
     "partial": dict(name="cfg3", nx=96, ny=80, nz=24, sweeps=18, mode=2, delta=6, recovery=1),
+    "periodic": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=1, bc=1),
+    "periodic_offline": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=2, delta=5,
+                             bc=1, recovery=1),
 }
 
 
