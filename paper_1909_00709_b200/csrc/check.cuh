@@ -326,6 +326,18 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
 #define ABFT_KU 4
 #endif
 constexpr int kCheckUnroll = ABFT_KU;
+// entries per thread in flight: the K2 round is memory-latency bound, so
+// few-point shapes take more entries per round; the 27-point prediction keeps
+// 27 terms per entry live and takes fewer (registers, occupancy)
+#ifndef ABFT_KU_FEW
+#define ABFT_KU_FEW 4
+#endif
+#ifndef ABFT_KU_MANY
+#define ABFT_KU_MANY 1
+#endif
+template <int S> constexpr int check_unroll() {
+  return (S == SHAPE_BOX27 || S == SHAPE_GENERIC) ? ABFT_KU_MANY : ABFT_KU_FEW;
+}
 
 // one vector (a' over x if A, else b' over y) of layer z: predict, store the
 // prediction (offline P / explicit check), compare with the actual checksum,
@@ -344,17 +356,18 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
   double* fwd0 = z == 0 ? (A ? p.fwdA[0] : p.fwdB[0]) : nullptr;
   double* fwd1 = z == p.zc - 1 ? (A ? p.fwdA[1] : p.fwdB[1]) : nullptr;
   const bool fwd_pred = p.flags & CK_STORE_PRED;
-  for (int e0 = lo + threadIdx.x; e0 < n; e0 += kCheckThreads * kCheckUnroll) {
-    double pr[kCheckUnroll], ac[kCheckUnroll];
+  constexpr int KU = check_unroll<S>();
+  for (int e0 = lo + threadIdx.x; e0 < n; e0 += kCheckThreads * KU) {
+    double pr[KU], ac[KU];
 #pragma unroll
-    for (int u = 0; u < kCheckUnroll; ++u) {
+    for (int u = 0; u < KU; ++u) {
       const int e = e0 + u * kCheckThreads;
       const bool in = e < n;
       pr[u] = in ? predict_entry<T, S, A, BCG>(p, z, e) : 0.0;
       ac[u] = (in && cmp) ? act[(size_t)bz * nn + e] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < kCheckUnroll; ++u) {
+    for (int u = 0; u < KU; ++u) {
       const int e = e0 + u * kCheckThreads;
       if (e >= n) break;
       if (p.flags & CK_STORE_PRED) pout[(size_t)bz * nn + e] = pr[u];
