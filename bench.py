@@ -291,8 +291,10 @@ def run_ours(a):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("config") == a.config and tj.get("policy", "lazy") == a.policy:
-                traffic = tj.get("dram_bytes_per_launch")
+            want = "offline" if pmode == 2 else a.policy
+            for e in (tj if isinstance(tj, list) else [tj]):
+                if e.get("config") == a.config and e.get("policy", "lazy") == want:
+                    traffic = e.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     launches = sum_over_ranks(rA["launches"], world)
