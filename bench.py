@@ -145,12 +145,17 @@ def timed(stream, fn):
     return e0.elapsed_time(e1)
 
 
+def _coll_device():
+    import torch.distributed as dist
+    return "cuda" if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(v: float, world: int) -> float:
-    return D.max_over_ranks(v, world, device="cuda")
+    return D.max_over_ranks(v, world, device=_coll_device())
 
 
 def sum_over_ranks(v: float, world: int) -> float:
-    return D.sum_over_ranks(v, world, device="cuda")
+    return D.sum_over_ranks(v, world, device=_coll_device())
 
 
 def barrier(world):
@@ -179,11 +184,18 @@ def run_ours(a):
     world, rank, local = dist_env()
     if a.gpus != world and world > 1:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE {world}")
+    # ABFT_BENCH_SHARE_GPU=1 (a check of the multi-rank path on a one-GPU box,
+    # not a measurement): every rank on cuda:0, gloo for the host collectives
+    share = os.environ.get("ABFT_BENCH_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     # N > 1: the z-slab halo moves over CUDA IPC by default -- the kernels store
     # it into the neighbours' mapped buffers (fused halo, NVLink); with
@@ -205,9 +217,16 @@ def run_ours(a):
         return dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
 
     def new_handle(*args, **kw):
+        nonlocal transport, nccl_id
         st = abft.from_problem(*args, **kw, **handle_kw())
-        if ipc_ctx is not None:
-            ipc_ctx.link(st)       # collective: every rank creates its handles in lockstep
+        if transport == "ipc" and not ipc_ctx.link(st):   # collective, lockstep on every rank
+            # IPC unavailable on some rank (no peer mapping): NCCL for the rest of the run
+            st.destroy()
+            import torch.distributed as dist
+            obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            transport, nccl_id = "nccl", obj[0]
+            st = abft.from_problem(*args, **kw, **handle_kw())
         return st
     p = make_problem(a.config)
     if not a.strong:            # weak scaling: each rank owns a slab of the config's size

@@ -55,6 +55,7 @@ extern "C" {
 #define ABFT_ECUDA (-3)               /* CUDA runtime / driver error */
 #define ABFT_ENCCL (-4)               /* NCCL error (nranks > 1) */
 #define ABFT_EUNSUPPORTED (-5)        /* valid per the paper but not implemented on this path */
+#define ABFT_ETIMEOUT (-6)            /* IPC job: a neighbour rank made no progress (ABFT_IPC_TIMEOUT_S) */
 
 /* ---- enums ---------------------------------------------------------------- */
 typedef enum { ABFT_F32 = 0, ABFT_F64 = 1 } abft_dtype;

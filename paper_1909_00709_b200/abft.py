@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libabft_stencil.so")
 
 ABFT_OK, ABFT_DETECTED_UNCORRECTABLE, ABFT_PERSISTENT_ERROR = 0, 1, 3
-ABFT_EINVAL, ABFT_ENOSPACE, ABFT_ECUDA, ABFT_ENCCL, ABFT_EUNSUPPORTED = -1, -2, -3, -4, -5
+ABFT_EINVAL, ABFT_ENOSPACE, ABFT_ECUDA, ABFT_ENCCL, ABFT_EUNSUPPORTED, ABFT_ETIMEOUT = -1, -2, -3, -4, -5, -6
 ABFT_F32, ABFT_F64 = 0, 1
 ABFT_BC_CLAMP, ABFT_BC_PERIODIC, ABFT_BC_ZERO, ABFT_BC_CONSTANT = 0, 1, 2, 3
 ABFT_MODE_NONE, ABFT_MODE_ONLINE, ABFT_MODE_OFFLINE = 0, 1, 2

@@ -8,6 +8,7 @@
 // missing device or driver entry point is a hard ABFT_ECUDA.
 #include <dlfcn.h>
 #include <sched.h>
+#include <time.h>
 #include <map>
 #include <array>
 #include <math.h>
@@ -634,6 +635,33 @@ void set_fwd(Group& G, const XSpec& x) {
 // s and enqueues a wait on the neighbour's event of parity s.  A neighbour
 // re-records that event only at exchange s + 2, which it reaches after this
 // rank published s + 1 -- i.e. after the wait below was enqueued.
+#define TRY(...)            \
+  do {                      \
+    int r_ = (__VA_ARGS__); \
+    if (r_) return r_;      \
+  } while (0)
+
+// Wait until a neighbour's progress word reaches `want`.  A rank that died or
+// never linked would leave the others spinning: give up after
+// ABFT_IPC_TIMEOUT_S seconds (default 120) with ABFT_ETIMEOUT.
+int ipc_wait(const volatile int64_t* word, int64_t want) {
+  static const double limit = [] {
+    const char* e = getenv("ABFT_IPC_TIMEOUT_S");
+    return e ? atof(e) : 120.0;
+  }();
+  if (__atomic_load_n(word, __ATOMIC_ACQUIRE) >= want) return ABFT_OK;
+  timespec t0, t;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (unsigned k = 0;; ++k) {
+    if (__atomic_load_n(word, __ATOMIC_ACQUIRE) >= want) return ABFT_OK;
+    if ((k & 1023) == 1023) {
+      clock_gettime(CLOCK_MONOTONIC, &t);
+      if ((t.tv_sec - t0.tv_sec) + 1e-9 * (t.tv_nsec - t0.tv_nsec) > limit) return ABFT_ETIMEOUT;
+    }
+    sched_yield();
+  }
+}
+
 int sync_ipc(abft_stencil* h) {
   on_dev(h);
   const int64_t s = ++h->xseq;
@@ -641,7 +669,7 @@ int sync_ipc(abft_stencil* h) {
   __atomic_store_n(&h->shm[h->cfg.rank].seq, s, __ATOMIC_RELEASE);
   for (abft_stencil* q : {h->lo_peer, h->hi_peer}) {
     if (!q) continue;
-    while (__atomic_load_n(&h->shm[q->cfg.rank].seq, __ATOMIC_ACQUIRE) < s) sched_yield();
+    TRY(ipc_wait(&h->shm[q->cfg.rank].seq, s));
     CK(cudaStreamWaitEvent(h->stream, q->ev_ipc[s & 1], 0));
   }
   return ABFT_OK;
@@ -675,11 +703,6 @@ int zero_gen(abft_stencil* h, int g, int za = 0, int zb = -1) {
   return ABFT_OK;
 }
 
-#define TRY(...)            \
-  do {                      \
-    int r_ = (__VA_ARGS__); \
-    if (r_) return r_;      \
-  } while (0)
 
 // one online sweep s = sweeps + 1 of every slab of the group: K1 (sweep +
 // actual checksums) then K2 (predict, compare, locate, correct, clear the
@@ -746,12 +769,12 @@ int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
   const int64_t w = ++h->wseq;
   const int n = h->cfg.nranks, me = h->cfg.rank, par = (int)(w & 1);
   for (int r = 0; r < n; ++r)
-    while (__atomic_load_n(&h->shm[r].wdone, __ATOMIC_ACQUIRE) < w - 2) sched_yield();
+    TRY(ipc_wait(&h->shm[r].wdone, w - 2));
   for (int k = 0; k < 3; ++k) h->shm[me].val[par][k] = d[k];
   __atomic_store_n(&h->shm[me].wseq, w, __ATOMIC_RELEASE);
   int m[3] = {0, 0, 0};
   for (int r = 0; r < n; ++r) {
-    while (__atomic_load_n(&h->shm[r].wseq, __ATOMIC_ACQUIRE) < w) sched_yield();
+    TRY(ipc_wait(&h->shm[r].wseq, w));
     for (int k = 0; k < 3; ++k) m[k] = std::max(m[k], h->shm[r].val[par][k]);
   }
   __atomic_store_n(&h->shm[me].wdone, w, __ATOMIC_RELEASE);
@@ -1058,6 +1081,7 @@ const char* abft_strerror(int s) {
     case ABFT_ECUDA: return "CUDA error";
     case ABFT_ENCCL: return "NCCL error";
     case ABFT_EUNSUPPORTED: return "unsupported by this build";
+    case ABFT_ETIMEOUT: return "timed out waiting for a neighbour rank (IPC)";
     default: return "unknown status";
   }
 }

@@ -57,7 +57,7 @@ def _rank_main(rank, world, port, pkw, faults, out_dir):
                                stream=torch.cuda.Stream(dev), z_begin=z0, z_count=zc, rank=rank,
                                nranks=world)
         st.set_faults([Fault(*f) for f in faults])
-        ctx.link(st)
+        assert ctx.link(st)
         status = st.step(p.sweeps)
         u = st.read_field().cpu().numpy()
         A, B = st.checksums()
