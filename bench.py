@@ -22,6 +22,7 @@ host buffers (pinned H2D of u0 and P, init, K sweeps, D2H of the field);
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -213,8 +214,13 @@ def run_ours(a):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
+    # online single slab: the checks of sweep s run beside sweep s + 1
+    # (abft_schedule AUTO, the default); ABFT_SCHEDULE=1 measures the serial order
+    sched = int(os.environ.get("ABFT_SCHEDULE", "0"))
+
     def handle_kw():
-        return dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id)
+        return dict(z_begin=z0, z_count=zc, rank=rank, nranks=world, nccl_unique_id=nccl_id,
+                    schedule=sched)
 
     def new_handle(*args, **kw):
         nonlocal transport, nccl_id
@@ -252,6 +258,9 @@ def run_ours(a):
         if with_faults:
             st.set_faults(shift(faults, W))
         st.step(W)
+        # single slab, error-free range: capture the CUDA graph of step(K) now
+        # (abft_stencil_plan; a no-op otherwise) -- the e2e job below pays it inside
+        st.plan(K)
         barrier(world)
         if prof:
             st.profile(True)
@@ -267,6 +276,14 @@ def run_ours(a):
         st.destroy()
         return out
 
+    # the schedule the library chose for this problem (abft_stencil_field_buffers:
+    # three buffers online = the checks of sweep s run beside sweep s + 1)
+    cfg_probe, _keep = abft.problem_config(p, P, z_begin=z0, z_count=zc, rank=rank, nranks=world,
+                                           schedule=sched)
+    nbuf = C.c_int32(0)
+    abft.lib().abft_stencil_field_buffers(C.byref(cfg_probe), C.byref(nbuf))
+    sched_label = ("pipelined: checks of sweep s beside sweep s + 1" if pmode == 1 and nbuf.value == 3
+                   else "serial: checks of sweep s before sweep s + 1")
     with torch.cuda.stream(stream):
         rA = protected_run(pmode, True)               # headline: flips on
         rE = protected_run(pmode, True, policy=pol_other)
@@ -382,6 +399,7 @@ def run_ours(a):
                        "nx": p.nx, "ny": p.ny, "nz": p.nz, "z_per_gpu": zc,
                        "parallelism": (f"z-slab x{world} ({'CUDA IPC fused halo' if transport == 'ipc' else 'NCCL halo'})"
                                        if world > 1 else "1 GPU"),
+                       "schedule": sched_label,
                        "l2": "inputs larger than L2 (4 GiB per array); no flush",
                        "k1_grid": list(prof["grid"]), "k1_threads": prof["threads"],
                        "k1_smem": prof["smem"], "k1_layers_per_cta": prof["zchunk"]},

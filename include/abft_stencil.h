@@ -91,6 +91,16 @@ typedef enum { ABFT_CK_BOTH = 0, ABFT_CK_LAZY = 1 } abft_checksum_policy;
  * (Q28).  Equal to ROLLBACK whenever every error of the window is
  * detected; an undetected one outside the range is not erased. */
 typedef enum { ABFT_RECOVER_ROLLBACK = 0, ABFT_RECOVER_PARTIAL = 1 } abft_recovery;
+/* Schedule of an ONLINE step() on a single slab (nranks == 1).  AUTO: when
+ * init is given a third field buffer, the checks of sweep s (steps (2)-(5))
+ * run on a side stream beside the stencil update of sweep s + 1, which reads
+ * u^s while it is being checked; a cell the checks rewrite is then recomputed
+ * in u^{s+1} (with its checksums) before anything reads u^{s+1}, so every
+ * result is bitwise that of the SERIAL order -- the paper's (fig.abft caption
+ * detect and correct after each sweep) -- and an error-free sweep
+ * never waits for its check.  SERIAL (or two buffers, or nranks > 1): each
+ * sweep's checks finish before the next sweep starts. */
+typedef enum { ABFT_SCHED_AUTO = 0, ABFT_SCHED_SERIAL = 1 } abft_schedule;
 /* abft_record.status */
 typedef enum {
   ABFT_REC_CORRECTED = 1,     /* located by intersection, corrected (Eq. 8)      */
@@ -156,7 +166,8 @@ typedef struct {
                                  for nranks == 1 or for a local group member (see
                                  abft_stencil_group) */
   int32_t recovery;     /* abft_recovery: what an OFFLINE dirty window re-executes */
-  int32_t pad;
+  int32_t schedule;     /* abft_schedule: how an ONLINE step() of a single slab
+                           orders the checks against the sweeps */
 } abft_config;
 
 /* A scheduled single bit-flip (fault model P:783-785): at sweep `sweep`
@@ -201,9 +212,18 @@ typedef struct abft_stencil abft_stencil;
  * invalid cfg, ABFT_EUNSUPPORTED for a valid one this build does not run. */
 int abft_stencil_workspace_size(const abft_config* cfg, size_t* field_bytes, size_t* aux_bytes);
 
+/* Number of field buffers init uses for `cfg` on the current device: 3 for
+ * OFFLINE (checkpoint rotation) and for an ONLINE single slab that runs the
+ * pipelined schedule (schedule AUTO and K1 z-chunks of at most two layers, or
+ * ABFT_PIPELINE=1), else 2.  Errors as abft_stencil_workspace_size, plus
+ * ABFT_ECUDA without a device. */
+int abft_stencil_field_buffers(const abft_config* cfg, int32_t* n);
+
 /* Create a handle.  field_bufs: 2 device buffers (NONE / ONLINE) or 3
- * (OFFLINE: the third holds the checkpoint, rotated without copies), each of
- * field_bytes; aux: device buffer of aux_bytes.  u0: this rank's initial
+ * (OFFLINE: the third holds the checkpoint, rotated without copies; ONLINE
+ * single slab with the pipelined schedule, see abft_stencil_field_buffers: the
+ * third keeps u^{s-1} for the checks of sweep s while sweep s + 1 runs -- NULL
+ * selects the serial schedule), each of field_bytes; aux: device buffer of aux_bytes.  u0: this rank's initial
  * slab, dense [z_count][ny][nx] of dtype, HOST or DEVICE pointer (copied).
  * stream: cudaStream_t to run on (NULL = default stream).  Computes the
  * trusted initial checksums a^0, b^0 and c_x, c_y, and (nranks > 1) creates
@@ -223,6 +243,17 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
  * window to read the verdict; returns ABFT_PERSISTENT_ERROR if a window
  * stayed dirty after its rollback. */
 int abft_stencil_step(abft_stencil* h, int32_t nsweeps);
+
+/* Prepare step(nsweeps) from the current state without running it.  A
+ * single-slab ONLINE (either schedule) or NONE step with no
+ * bit-flip scheduled in its range, runs as one CUDA graph: the launch
+ * sequence depends only on the rotation phase (field buffer, checksum
+ * generation, sweep parity), so step() captures it on first use and replays
+ * it whenever the phase and length recur (up to 8 cached per handle).  plan()
+ * does that capture ahead of time, so the first step() of that phase does not
+ * pay it.  A no-op (ABFT_OK) for any other step.  ABFT_GRAPHS=0 in the
+ * environment disables the graphs (every call enqueued directly). */
+int abft_stencil_plan(abft_stencil* h, int32_t nsweeps);
 
 /* Local group: n handles created by THIS process for the n slabs of one
  * domain (cfg.nranks = n, cfg.rank = i, cfg.nccl_unique_id = NULL, slabs

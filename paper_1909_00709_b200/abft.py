@@ -15,12 +15,15 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libabft_stencil.so")
+if os.environ.get("ABFT_LIB"):   # A/B experiments against another build (tools/)
+    LIB_PATH = os.environ["ABFT_LIB"]
 
 ABFT_OK, ABFT_DETECTED_UNCORRECTABLE, ABFT_PERSISTENT_ERROR = 0, 1, 3
 ABFT_EINVAL, ABFT_ENOSPACE, ABFT_ECUDA, ABFT_ENCCL, ABFT_EUNSUPPORTED, ABFT_ETIMEOUT = -1, -2, -3, -4, -5, -6
 ABFT_F32, ABFT_F64 = 0, 1
 ABFT_BC_CLAMP, ABFT_BC_PERIODIC, ABFT_BC_ZERO, ABFT_BC_CONSTANT = 0, 1, 2, 3
 ABFT_MODE_NONE, ABFT_MODE_ONLINE, ABFT_MODE_OFFLINE = 0, 1, 2
+ABFT_SCHED_AUTO, ABFT_SCHED_SERIAL = 0, 1
 ABFT_CK_BOTH, ABFT_CK_LAZY = 0, 1
 ABFT_RECOVER_ROLLBACK, ABFT_RECOVER_PARTIAL = 0, 1
 REC_CORRECTED, REC_UNLOCATED, REC_UNCORRECTABLE, REC_WINDOW_DIRTY, REC_PERSISTENT, REC_RECOMPUTED, REC_VERIFIED = 1, 2, 3, 4, 5, 6, 7
@@ -32,7 +35,8 @@ EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_ste
            "abft_stencil_status", "abft_stencil_sweep_count", "abft_stencil_launch_count",
            "abft_stencil_destroy", "abft_strerror", "abft_stencil_profile",
            "abft_stencil_profile_read", "abft_stencil_group", "abft_stencil_step_group",
-           "abft_stencil_halo_plan", "abft_stencil_ipc_export", "abft_stencil_ipc_link")
+           "abft_stencil_halo_plan", "abft_stencil_ipc_export", "abft_stencil_ipc_link",
+           "abft_stencil_plan", "abft_stencil_field_buffers")
 IPC_BLOB_BYTES = 1024
 
 
@@ -54,7 +58,7 @@ class abft_config(C.Structure):
                 ("epsilon", C.c_double), ("mode", C.c_int32), ("delta", C.c_int32),
                 ("correction_form", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("checksum_policy", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("recovery", C.c_int32), ("pad", C.c_int32)]
+                ("recovery", C.c_int32), ("schedule", C.c_int32)]
 
 
 class abft_fault(C.Structure):
@@ -103,6 +107,8 @@ def lib() -> C.CDLL:
         L.abft_stencil_workspace_size.argtypes = [cfgp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
         L.abft_stencil_init.argtypes = [cfgp, C.POINTER(vp), vp, vp, vp, C.POINTER(vp)]
         L.abft_stencil_step.argtypes = [vp, i32]
+        L.abft_stencil_plan.argtypes = [vp, i32]
+        L.abft_stencil_field_buffers.argtypes = [cfgp, C.POINTER(i32)]
         L.abft_stencil_sweep.argtypes = [vp]
         L.abft_stencil_check.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
         L.abft_stencil_correct.argtypes = [vp, C.POINTER(i64)]
@@ -157,7 +163,7 @@ def make_config(nx: int, ny: int, nz: int, dtype, points: Sequence[Tuple[int, in
                 mode: int = ABFT_MODE_ONLINE, delta: int = 1, correction_form: int = 0,
                 z_begin: int = 0, z_count: Optional[int] = None, rank: int = 0,
                 nranks: int = 1, nccl_unique_id: Optional[bytes] = None,
-                checksum_policy: int = 0, recovery: int = 0):
+                checksum_policy: int = 0, recovery: int = 0, schedule: int = 0):
     """abft_config for the problem as the paper states it (Eq. 1: stencil points
     (di, dj, dk, w) in evaluation order + constant-term sources
     (coef, device field or None, scalar); BC; threshold; offline period).
@@ -184,6 +190,7 @@ def make_config(nx: int, ny: int, nz: int, dtype, points: Sequence[Tuple[int, in
     c.rank, c.nranks = rank, nranks
     c.checksum_policy = checksum_policy
     c.recovery = recovery
+    c.schedule = schedule
     idbuf = None
     if nccl_unique_id is not None:
         idbuf = C.create_string_buffer(bytes(nccl_unique_id), 128)
@@ -221,7 +228,12 @@ class Stencil:
         self.dtype = torch.float32 if cfg.dtype == ABFT_F32 else torch.float64
         self.shape = (cfg.z_count, cfg.ny, cfg.nx)
         fb, ab = abft_stencil_workspace_size(cfg)
-        nbuf = 3 if cfg.mode == ABFT_MODE_OFFLINE else 2
+        # offline: the checkpoint; pipelined online schedule: u^{s-1} for the
+        # checks running beside the next sweep
+        nb = C.c_int32(2)
+        with torch.cuda.device(self.device):
+            _ok("abft_stencil_field_buffers", lib().abft_stencil_field_buffers(C.byref(cfg), C.byref(nb)))
+        nbuf = nb.value
         self.fields = [torch.empty(fb, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
         self.aux = torch.empty(ab, dtype=torch.uint8, device=self.device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -251,6 +263,10 @@ class Stencil:
     # -- run ---------------------------------------------------------------
     def step(self, n: int) -> int:
         return _ok("abft_stencil_step", lib().abft_stencil_step(self.h, n), allow_positive=True)
+
+    def plan(self, n: int) -> None:
+        """abft_stencil_plan: capture the graph of step(n) from the current state."""
+        _ok("abft_stencil_plan", lib().abft_stencil_plan(self.h, n))
 
     def sweep(self) -> None:
         _ok("abft_stencil_sweep", lib().abft_stencil_sweep(self.h))

@@ -146,12 +146,59 @@ struct Layout {
   int64_t px, plane;
   size_t field_bytes;
   // aux offsets
-  size_t off_gA[3], off_gB[3], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_lazy, off_st, off_src;
+  size_t off_gA[kGens], off_gB[kGens], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_lazy, off_st, off_src;
   size_t off_EX[3];  // x-edge ledger of each field buffer, [2][zc+2][ny] of dtype
   size_t aux_bytes;
   size_t hot_bytes;  // prefix of aux touched every sweep
   bool pad_src;
 };
+
+// K1 launch geometry of a config on a device, and whether an online step()
+// runs the pipelined schedule
+struct K1Plan {
+  int zchunk;
+  dim3 grid;
+  bool pipe;
+};
+K1Plan k1_plan(const abft_config* cfg, int dev) {
+  const K1Geometry geo = k1_geometry(cfg->dtype);
+  const int64_t nx = cfg->nx, ny = cfg->ny, zc = cfg->z_count;
+  int nsm = 148;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
+  const int tiles_x = (int)((nx + geo.tile_x - 1) / geo.tile_x);
+  const int tiles_y = (int)((ny + geo.tile_y - 1) / geo.tile_y);
+  const int64_t tiles = (int64_t)tiles_x * tiles_y;
+  // z-chunks: ~32 waves of resident CTAs (the last, partial wave then costs
+  // little; measured on cfg4: 8 waves / 103 layers per CTA -> 32 waves / 28
+  // layers: protected K1 -3%), but >= 16 layers per CTA (each chunk re-stages
+  // its two z-halo layers)
+  const int per_sm = std::max(1, (228 * 1024) / (geo.smem + 1024));
+  const int64_t target = (int64_t)32 * nsm * per_sm;
+  int64_t nch = std::max<int64_t>(1, std::min<int64_t>(zc, (target + tiles - 1) / tiles));
+  int64_t zch = std::max<int64_t>((zc + nch - 1) / nch, std::min<int64_t>(zc, 16));
+  // ... unless that leaves SMs idle (few tiles and layers: cfg2, cfg3), then
+  // about four waves of short chunks (cfg3: 13 -> 4 layers per CTA measured
+  // 42.2 -> 37.2 us per unprotected sweep; cfg2 stays at 1)
+  const int64_t slots = (int64_t)nsm * per_sm;
+  if (tiles * ((zc + zch - 1) / zch) < slots)
+    zch = std::max<int64_t>(1, (tiles * zc + 4 * slots - 1) / (4 * slots));
+  K1Plan k;
+  k.zchunk = (int)zch;
+  if (const char* e = getenv("ABFT_ZCHUNK")) k.zchunk = std::max(1, std::min((int)zc, atoi(e)));
+  k.grid = dim3(tiles_x, tiles_y, (unsigned)((zc + k.zchunk - 1) / k.zchunk));
+  // The pipelined schedule pays where K1's CTAs are short-lived (one or two
+  // layers each: cfg1, cfg2): the checks' CTAs get SM slots as K1's retire.
+  // With long z-chunks K1 holds every slot (two CTAs use the whole register
+  // file) until its last wave, so the checks cannot run beside it and the
+  // serial order is as fast or faster (measured).
+  // ABFT_PIPELINE=0/1 overrides the choice where the schedule is allowed.
+  k.pipe = cfg->mode == ABFT_MODE_ONLINE && cfg->nranks == 1 && cfg->schedule == ABFT_SCHED_AUTO;
+  if (k.pipe) {
+    const char* e = getenv("ABFT_PIPELINE");
+    k.pipe = e ? atoi(e) != 0 : k.zchunk <= 2;
+  }
+  return k;
+}
 
 int field_source(const abft_config* c) {
   int fs = -1;
@@ -189,6 +236,7 @@ int validate(const abft_config* c) {
   if (c->correction_form < 0 || c->correction_form > 2) return ABFT_EINVAL;
   if (c->checksum_policy != ABFT_CK_BOTH && c->checksum_policy != ABFT_CK_LAZY) return ABFT_EINVAL;
   if (c->recovery != ABFT_RECOVER_ROLLBACK && c->recovery != ABFT_RECOVER_PARTIAL) return ABFT_EINVAL;
+  if (c->schedule != ABFT_SCHED_AUTO && c->schedule != ABFT_SCHED_SERIAL) return ABFT_EINVAL;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return ABFT_EINVAL;
   if (c->nranks > 1) {
     if ((c->rank == 0) != (c->z_begin == 0)) return ABFT_EINVAL;
@@ -213,7 +261,7 @@ Layout layout(const abft_config* c) {
   // per-sweep vectors first (checksum generations, c_x / c_y, edge ledgers).
   // A persisting-L2 window over them was measured: K2 unchanged, K1 2x slower
   // (the carve-out starves the streaming sweep), so none is set.
-  for (int g = 0; g < 3; ++g) { L.off_gA[g] = take(zc2 * c->nx * 8); L.off_gB[g] = take(zc2 * c->ny * 8); }
+  for (int g = 0; g < kGens; ++g) { L.off_gA[g] = take(zc2 * c->nx * 8); L.off_gB[g] = take(zc2 * c->ny * 8); }
   L.off_cA = take((size_t)c->z_count * c->nx * 8);
   L.off_cB = take((size_t)c->z_count * c->ny * 8);
   for (int b = 0; b < 3; ++b) L.off_EX[b] = take((size_t)2 * zc2 * c->ny * L.esz);
@@ -240,6 +288,28 @@ struct PendingFault {
 struct abft_stencil;
 using Group = std::vector<abft_stencil*>;
 
+namespace {
+// A whole step(n) of a single slab captured as one CUDA graph.  What a step
+// enqueues depends only on the rotation phase (field buffer, checksum
+// generation, sweep parity, generations known zero) and n, so a later call in
+// the same phase replays the instantiated graph; the sweep numbers the checks
+// record are offset on the device (DevState::sweep_off, set by the graph's
+// first node).
+struct StepGraph {
+  int n, cur, gen, par;
+  unsigned zmask;
+  int64_t sweeps0;                 // sweep count at capture
+  cudaGraph_t graph = nullptr;     // kept: its node handles address the exec's nodes
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t off = nullptr;   // memset node: sweep_off = sweeps - sweeps0
+  int cur2, prev2, gen2, gen_prev2;
+  unsigned zmask2;
+  int64_t launches;
+  uint64_t used;
+};
+constexpr size_t kMaxGraphs = 8;
+}  // namespace
+
 struct abft_stencil {
   abft_config cfg;
   std::vector<abft_point> points;
@@ -249,8 +319,8 @@ struct abft_stencil {
   char* fb[3] = {nullptr, nullptr, nullptr};
   char* aux = nullptr;
   char* EX[3] = {nullptr, nullptr, nullptr};
-  double* gA[3];
-  double* gB[3];
+  double* gA[kGens];
+  double* gB[kGens];
   double* PA[2];
   double* PB[2];
   double *cA, *cB;
@@ -275,7 +345,7 @@ struct abft_stencil {
   int gen = 0;       // checksum generation of the current state
   int gen_prev = 0;
   bool pending_check = false;
-  bool next_zero = true;  // generation (gen + 1) % 3 is known to be zero
+  unsigned zmask = 0;      // bit g: checksum generation g is known to be zero
   bool summ_dirty = false; // check() left layer summaries that correct() did not consume
   int64_t sweeps = 0;      // logical sweep index of the current state
   int64_t executed = 0;    // sweeps executed, incl. re-executions after rollbacks
@@ -306,6 +376,16 @@ struct abft_stencil {
   int fwd_buf = -1, fwd_kind = 0, fwd_idx = 0;
   int dev = 0;
   cudaEvent_t ev_ready = nullptr, ev_pulled = nullptr;
+  // pipelined online schedule (single slab, three field buffers): the checks
+  // of sweep s on the side stream s2, beside K1 of sweep s + 1 (online_pipelined)
+  bool pipe = false;
+  cudaStream_t s2 = nullptr;
+  cudaStream_t cs = nullptr;        // capture stream of the step graphs
+  bool graphs_on = true;            // ABFT_GRAPHS=0: enqueue every call directly
+  bool pipe_pdl = false;            // pipelined K1 with programmatic serialization (experiment)
+  std::vector<StepGraph> graphs;
+  uint64_t graph_tick = 0;
+  cudaEvent_t ev_k1 = nullptr, ev_chk[2] = {nullptr, nullptr};
   // measurement hook: event pairs around K1 / K2 launches
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -331,7 +411,7 @@ struct DevScope {
   ~DevScope() { if (old >= 0) cudaSetDevice(old); }
 };
 
-cudaEvent_t* prof_begin(abft_stencil* h, int kind) {
+cudaEvent_t* prof_begin(abft_stencil* h, int kind, cudaStream_t s) {
   if (!h->prof) return nullptr;
   if (h->ev_used * 2 + 2 > h->ev.size()) {
     for (int i = 0; i < 2; ++i) {
@@ -344,11 +424,11 @@ cudaEvent_t* prof_begin(abft_stencil* h, int kind) {
   cudaEvent_t* pair = &h->ev[h->ev_used * 2];
   h->ev_kind[h->ev_used] = kind;
   h->ev_used++;
-  cudaEventRecord(pair[0], h->stream);
+  cudaEventRecord(pair[0], s);
   return pair;
 }
-void prof_end(abft_stencil* h, cudaEvent_t* pair) {
-  if (pair) cudaEventRecord(pair[1], h->stream);
+void prof_end(cudaEvent_t* pair, cudaStream_t s) {
+  if (pair) cudaEventRecord(pair[1], s);
 }
 
 #define CK(x)                                              \
@@ -415,11 +495,36 @@ CheckParams make_check(abft_stencil* h, int uprev, int ucur, const double* Ap, c
   return p;
 }
 
+// this slab's armed flips of `sweep` (at most one per cell per execution);
+// `mark`: they fire now
+int sweep_faults(abft_stencil* h, int64_t sweep, LocalFault* out, bool mark) {
+  int n = 0;
+  for (auto& pf : h->faults) {
+    if (pf.fired || pf.f.sweep != sweep) continue;
+    const int64_t zl = pf.f.z - h->cfg.z_begin;
+    if (zl < 0 || zl >= h->cfg.z_count) continue;
+    bool dup = false;
+    for (int k = 0; k < n; ++k)
+      if (out[k].z == zl && out[k].y == pf.f.y && out[k].x == pf.f.x) dup = true;
+    if (dup || n == kMaxFaultsPerLaunch) continue;
+    out[n++] = LocalFault{(int)zl, (int)pf.f.y, (int)pf.f.x, pf.f.bit};
+    if (mark) pf.fired = true;
+  }
+  return n;
+}
+
+// CTAs of a whole-slab K1 launch
+unsigned long long k1_grid_ctas(const abft_stencil* h) {
+  const unsigned long long gz = (h->cfg.z_count + h->zchunk - 1) / h->zchunk;
+  return (unsigned long long)h->grid1.x * h->grid1.y * gz;
+}
+
 // K1: step (1)
 // za / zb: the slab-local layers [za, zb) to compute (partial re-execution;
-// zb < 0: the whole slab)
+// zb < 0: the whole slab); count: add its CTAs to DevState::k1_cnt[sweep & 1] as they
+// finish (pipelined schedule)
 int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, int64_t sweep,
-              int za = 0, int zb = -1) {
+              int za = 0, int zb = -1, bool count = false) {
   SweepParams p = h->sp;
   if (zb < 0) zb = (int)h->cfg.z_count;
   p.zr0 = za;
@@ -437,53 +542,45 @@ int launch_k1(abft_stencil* h, int src, int dst, double* A, double* B, int chk, 
   p.EX = h->cfg.mode != ABFT_MODE_NONE ? h->EX[dst] : nullptr;
   p.A = A;
   p.B = B;
-  p.nfaults = 0;
-  // this sweep's armed faults in the slab: at most one per cell per execution
-  for (auto& pf : h->faults) {
-    if (pf.fired || pf.f.sweep != sweep) continue;
-    const int64_t zl = pf.f.z - h->cfg.z_begin;
-    if (zl < 0 || zl >= h->cfg.z_count) continue;
-    bool dup = false;
-    for (int k = 0; k < p.nfaults; ++k)
-      if (p.faults[k].z == zl && p.faults[k].y == pf.f.y && p.faults[k].x == pf.f.x) dup = true;
-    if (dup || p.nfaults == kMaxFaultsPerLaunch) continue;
-    p.faults[p.nfaults++] = LocalFault{(int)zl, (int)pf.f.y, (int)pf.f.x, pf.f.bit};
-    pf.fired = true;
-  }
+  p.done = count ? &h->st->k1_cnt[sweep & 1] : nullptr;
+  p.nfaults = sweep_faults(h, sweep, p.faults, true);
   // K1 variant: constant / periodic ghosts need the general one; scheduled
   // flips the injecting one; everything else runs the hot path
   const bool inj = p.nfaults > 0;
   on_dev(h);
-  const int var = (h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC) ? K1_GEN
-                  : (inj ? K1_INJ : K1_HOT);
+  const int var = ((h->cfg.bc == ABFT_BC_CONSTANT || h->cfg.bc == ABFT_BC_PERIODIC) ? K1_GEN
+                   : (inj ? K1_INJ : K1_HOT)) | (count && !h->pipe_pdl ? K1_NO_PDL : 0);
   h->executed++;
-  cudaEvent_t* pe = prof_begin(h, 1);
+  cudaEvent_t* pe = prof_begin(h, 1, h->stream);
   const cudaError_t e = h->cfg.dtype == ABFT_F32
             ? launch_k1_f32(h->shape, chk, var, grid, h->stream, h->tm_u[src], p)
             : launch_k1_f64(h->shape, chk, var, grid, h->stream, h->tm_u[src], p);
-  prof_end(h, pe);
+  prof_end(pe, h->stream);
   h->launches++;
   CK(e);
   return ABFT_OK;
 }
 
-// K2: steps (2)-(5) as their own launch
-int launch_check(abft_stencil* h, const CheckParams& p) {
+// K2: steps (2)-(5) as their own launch (on the handle's stream, or the
+// side stream of the pipelined schedule)
+int launch_check(abft_stencil* h, const CheckParams& p, cudaStream_t s = nullptr) {
   on_dev(h);
-  cudaEvent_t* pe = prof_begin(h, 2);
-  cudaError_t e = launch_k2(h->cfg.dtype, h->shape, h->stream, p);
-  prof_end(h, pe);
+  if (!s) s = h->stream;
+  cudaEvent_t* pe = prof_begin(h, 2, s);
+  cudaError_t e = launch_k2(h->cfg.dtype, h->shape, s, p);
+  prof_end(pe, s);
   h->launches++;
   CK(e);
   return ABFT_OK;
 }
 
 // K3 (lazy policy): a vectors + locate / correct of the layers K2 handed over
-int launch_lazy(abft_stencil* h, const CheckParams& p) {
+int launch_lazy(abft_stencil* h, const CheckParams& p, cudaStream_t s = nullptr) {
   on_dev(h);
-  cudaEvent_t* pe = prof_begin(h, 2);
-  cudaError_t e = launch_k3(h->cfg.dtype, h->shape, h->stream, p);
-  prof_end(h, pe);
+  if (!s) s = h->stream;
+  cudaEvent_t* pe = prof_begin(h, 2, s);
+  cudaError_t e = launch_k3(h->cfg.dtype, h->shape, s, p);
+  prof_end(pe, s);
   h->launches++;
   CK(e);
   return ABFT_OK;
@@ -690,10 +787,24 @@ int halo_exchange(Group& G, const XSpec& x) {
   return exchange_nccl(h, x);
 }
 
+int zero_gen(abft_stencil* h, int g, int za = 0, int zb = -1);
+// the buffer an online / unprotected sweep writes (three rotate on a
+// pipelined handle, so u^{s-1} survives the next sweep)
+int next_buf(const abft_stencil* h) { return h->nbuf == 3 ? (h->cur + 1) % 3 : 1 - h->cur; }
+// K1 accumulates into generation g: clear it first unless it is known zero
+int take_gen(abft_stencil* h, int g) {
+  if (!((h->zmask >> g) & 1u)) {
+    int r = zero_gen(h, g);
+    if (r) return r;
+  }
+  h->zmask &= ~(1u << g);
+  return ABFT_OK;
+}
+
 // the interior rows of a checksum generation, which K1 accumulates into; the
 // halo rows belong to the neighbours' exchange (a fused neighbour may already
 // have written them on its own stream)
-int zero_gen(abft_stencil* h, int g, int za = 0, int zb = -1) {
+int zero_gen(abft_stencil* h, int g, int za, int zb) {
   on_dev(h);
   const int64_t nx = h->cfg.nx, ny = h->cfg.ny;
   if (zb < 0) zb = (int)h->cfg.z_count;
@@ -710,11 +821,11 @@ int zero_gen(abft_stencil* h, int g, int za = 0, int zb = -1) {
 int online_sweep(Group& G) {
   abft_stencil* h0 = G[0];
   const int64_t s = h0->sweeps + 1;
-  const int src = h0->cur, dst = 1 - h0->cur;
-  const int gp = h0->gen, gn = (h0->gen + 1) % 3, gz = (h0->gen + 2) % 3;
+  const int src = h0->cur, dst = next_buf(h0);
+  const int gp = h0->gen, gn = (h0->gen + 1) % kGens, gz = (h0->gen + 2) % kGens;
   set_fwd(G, XSpec{dst, XV_GEN, gn});
   for (abft_stencil* h : G) {
-    if (!h->next_zero) TRY(zero_gen(h, gn));
+    TRY(take_gen(h, gn));
     if (h->cfg.checksum_policy == ABFT_CK_LAZY) {
       // b in the pass; a (generations used as scratch) by K3 only
       // for layers whose b flagged
@@ -738,8 +849,63 @@ int online_sweep(Group& G) {
     h->gen_prev = gp;
     h->gen = gn;
     h->sweeps = s;
-    h->next_zero = true;  // K2 cleared generation gz = (gn + 1) % 3
+    h->zmask |= 1u << gz;  // K2 cleared the generation of sweep s + 1
   }
+  return ABFT_OK;
+}
+
+// Pipelined online schedule (single slab, three field buffers):
+// K1 of sweep s + 1 is launched right behind K1 of sweep s, and the checks of
+// sweep s (K2, and K3 under LAZY) run beside it on the side stream.  They
+// read u^{s-1} (the third buffer, which K1 of s + 1 does not write) and u^s,
+// and K1 of s + 2 waits for them (it overwrites u^{s-1} and accumulates into
+// the generation they cleared).  A cell of u^s the checks rewrite may already
+// have been read by K1 of s + 1: the kernel that finishes the checks then
+// recomputes the cells of u^{s+1} that read it (fix_next), so the result is
+// bitwise the serial schedule's -- the paper's order -- while error-free
+// sweeps never wait for a check.
+int online_pipelined(abft_stencil* h, int32_t n) {
+  on_dev(h);
+  const bool lazy = h->cfg.checksum_policy == ABFT_CK_LAZY;
+  for (int i = 0; i < n; ++i) {
+    const int64_t s = h->sweeps + 1;
+    const int src = h->cur, dst = (h->cur + 1) % 3;
+    const int gp = h->gen, gn = (gp + 1) % kGens, g1 = (gp + 2) % kGens, g2 = (gp + 3) % kGens;
+    TRY(take_gen(h, gn));
+    // after the checks of sweep s - 2 (the previous call's are complete)
+    if (i >= 2) CK(cudaStreamWaitEvent(h->stream, h->ev_chk[s & 1], 0));
+    TRY(launch_k1(h, src, dst, lazy ? nullptr : h->gA[gn], h->gB[gn], lazy ? K1_CK_B : K1_CK_AB, s, 0, -1,
+                  true));
+    CK(cudaEventRecord(h->ev_k1, h->stream));
+    CK(cudaStreamWaitEvent(h->s2, h->ev_k1, 0));
+    // the checks of s clear the generation of sweep s + 2
+    CheckParams ck = make_check(h, src, dst, h->gA[gp], h->gB[gp], h->gA[gn], h->gB[gn], nullptr, nullptr,
+                                lazy ? nullptr : h->gA[g2], h->gB[g2],
+                                CK_COMPARE | CK_CORRECT | (lazy ? CK_LAZY : 0), s);
+    if (lazy) ck.Aw = h->gA[gp];
+    ck.k1_reset = 1;
+    if (i + 1 < n) {   // K1 of s + 1 will be in flight beside these checks
+      const int nb = (dst + 1) % 3;
+      ck.fix = 1;
+      ck.k1_target = (unsigned)k1_grid_ctas(h);
+      ck.unext = h->fb[nb];
+      ck.Anext = lazy ? nullptr : h->gA[g1];
+      ck.Bnext = h->gB[g1];
+      ck.EXnext = h->EX[nb];
+      ck.nfn = sweep_faults(h, s + 1, ck.fn, false);
+    }
+    TRY(launch_check(h, ck, h->s2));
+    if (lazy) TRY(launch_lazy(h, ck, h->s2));
+    CK(cudaEventRecord(h->ev_chk[s & 1], h->s2));
+    h->zmask |= 1u << g2;
+    h->prev = src;
+    h->cur = dst;
+    h->gen_prev = gp;
+    h->gen = gn;
+    h->sweeps = s;
+  }
+  // the caller's stream orders everything after the last check
+  if (n > 0) CK(cudaStreamWaitEvent(h->stream, h->ev_chk[h->sweeps & 1], 0));
   return ABFT_OK;
 }
 
@@ -872,7 +1038,7 @@ int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, 
 // persistent error.
 int offline_window(Group& G, int L) {
   abft_stencil* h0 = G[0];
-  const int ck = h0->cur, ckgen = h0->gen, gend = (h0->gen + 1) % 3;
+  const int ck = h0->cur, ckgen = h0->gen, gend = (h0->gen + 1) % kGens;
   const int64_t s0 = h0->sweeps;
   const bool partial = h0->cfg.recovery == ABFT_RECOVER_PARTIAL;
   int others[2], k = 0;
@@ -948,7 +1114,7 @@ int offline_window(Group& G, int L) {
     h->cur = last;
     h->gen_prev = ckgen;
     h->gen = gend;
-    h->next_zero = false;
+    h->zmask &= ~(1u << gend);
   }
   return worst;
 }
@@ -959,6 +1125,144 @@ int clear_summaries(abft_stencil* h) {
     CK(cudaMemsetAsync(h->summ, 0, sizeof(LayerSummary) * h->cfg.z_count, h->stream));
     h->summ_dirty = false;
   }
+  return ABFT_OK;
+}
+
+// ---------------------------------------------------------- step graphs
+// a step of this handle that may run as a captured graph: one slab, the
+// pipelined online schedule or unprotected sweeps, no flip scheduled in the
+// range (flips change the launch parameters; those calls enqueue directly)
+bool graph_eligible(const abft_stencil* h, int32_t n) {
+  if (!h->graphs_on || h->prof || n < 1 || h->grouped || h->ipc || h->cfg.nranks != 1) return false;
+  if (h->cfg.mode == ABFT_MODE_OFFLINE) return false;   // one host verdict per window
+  for (const PendingFault& pf : h->faults)
+    if (!pf.fired && pf.f.sweep > h->sweeps && pf.f.sweep <= h->sweeps + n + 1) return false;
+  return true;
+}
+
+StepGraph* graph_find(abft_stencil* h, int32_t n) {
+  for (StepGraph& g : h->graphs)
+    if (g.n == n && g.cur == h->cur && g.gen == h->gen && g.par == (int)(h->sweeps & 1) && g.zmask == h->zmask)
+      return &g;
+  return nullptr;
+}
+
+int run_direct(abft_stencil* h, int32_t n);
+
+// the sweep-offset memset node on stream st (inside a capture)
+int offset_node(abft_stencil* h, cudaStream_t st, cudaGraphNode_t* out) {
+  cudaStreamCaptureStatus cst;
+  cudaGraph_t cg;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, &deps, &nd));
+  cudaMemsetParams mp = {};
+  mp.dst = &h->st->sweep_off;
+  mp.value = 0;
+  mp.elementSize = 4;
+  mp.width = 1;
+  mp.height = 1;
+  mp.pitch = 4;
+  CK(cudaGraphAddMemsetNode(out, cg, deps, nd, &mp));
+  CK(cudaStreamUpdateCaptureDependencies(st, out, 1, cudaStreamSetCaptureDependencies));
+  return ABFT_OK;
+}
+
+// capture step(n) from the current state (which is left unchanged)
+int graph_capture(abft_stencil* h, int32_t n, StepGraph** out) {
+  on_dev(h);
+  if (!h->cs && cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking) != cudaSuccess) return ABFT_ECUDA;
+  StepGraph g;
+  g.n = n; g.cur = h->cur; g.gen = h->gen; g.par = (int)(h->sweeps & 1); g.zmask = h->zmask;
+  g.sweeps0 = h->sweeps;
+  const int prev0 = h->prev, gen_prev0 = h->gen_prev;
+  const int64_t sweeps0 = h->sweeps, executed0 = h->executed, launches0 = h->launches;
+  cudaStream_t user = h->stream;
+  h->stream = h->cs;
+  cudaGraph_t graph = nullptr;
+  int r = ABFT_OK;
+  if (cudaStreamBeginCapture(h->cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) r = ABFT_ECUDA;
+  if (r == ABFT_OK && h->pipe) {   // records of this graph's checks: sweep numbers offset per replay
+    if (cudaEventRecord(h->ev_k1, h->cs) != cudaSuccess || cudaStreamWaitEvent(h->s2, h->ev_k1, 0) != cudaSuccess)
+      r = ABFT_ECUDA;
+    if (r == ABFT_OK) r = offset_node(h, h->s2, &g.off);
+  } else if (r == ABFT_OK && h->cfg.mode == ABFT_MODE_ONLINE) {
+    r = offset_node(h, h->cs, &g.off);
+  }
+  if (r == ABFT_OK) r = run_direct(h, n);
+  if (r == ABFT_OK && h->pipe) {   // back to 0 for calls enqueued directly
+    cudaGraphNode_t z;
+    if (cudaStreamWaitEvent(h->s2, h->ev_chk[h->sweeps & 1], 0) != cudaSuccess) r = ABFT_ECUDA;
+    if (r == ABFT_OK) r = offset_node(h, h->s2, &z);
+    if (r == ABFT_OK && (cudaEventRecord(h->ev_k1, h->s2) != cudaSuccess ||
+                         cudaStreamWaitEvent(h->cs, h->ev_k1, 0) != cudaSuccess))
+      r = ABFT_ECUDA;
+  } else if (r == ABFT_OK && h->cfg.mode == ABFT_MODE_ONLINE) {
+    cudaGraphNode_t z;
+    r = offset_node(h, h->cs, &z);
+  }
+  const cudaError_t ee = cudaStreamEndCapture(h->cs, &graph);
+  if (r == ABFT_OK && ee != cudaSuccess) r = ABFT_ECUDA;
+  if (r == ABFT_OK) {
+    cudaGraphExec_t ex = nullptr;
+    if (cudaGraphInstantiate(&ex, graph, 0) != cudaSuccess) r = ABFT_ECUDA;
+    g.exec = ex;
+    // the device-side copy of the graph now, not at its first launch
+    if (r == ABFT_OK && cudaGraphUpload(ex, user) != cudaSuccess) r = ABFT_ECUDA;
+  }
+  g.graph = graph;
+  g.cur2 = h->cur; g.prev2 = h->prev; g.gen2 = h->gen; g.gen_prev2 = h->gen_prev; g.zmask2 = h->zmask;
+  g.launches = h->launches - launches0;
+  // the state as before: the graph runs when launched
+  h->stream = user;
+  h->cur = g.cur; h->prev = prev0; h->gen = g.gen; h->gen_prev = gen_prev0; h->zmask = g.zmask;
+  h->sweeps = sweeps0; h->executed = executed0; h->launches = launches0;
+  if (r != ABFT_OK) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    cudaGetLastError();
+    return r;
+  }
+  if (h->graphs.size() >= kMaxGraphs) {   // evict the least recently used
+    size_t v = 0;
+    for (size_t i = 1; i < h->graphs.size(); ++i)
+      if (h->graphs[i].used < h->graphs[v].used) v = i;
+    cudaGraphExecDestroy(h->graphs[v].exec);
+    cudaGraphDestroy(h->graphs[v].graph);
+    h->graphs.erase(h->graphs.begin() + v);
+  }
+  g.used = ++h->graph_tick;
+  h->graphs.push_back(g);
+  *out = &h->graphs.back();
+  return ABFT_OK;
+}
+
+int graph_launch(abft_stencil* h, StepGraph* g) {
+  on_dev(h);
+  if (g->off) {
+    cudaMemsetParams mp = {};
+    mp.dst = &h->st->sweep_off;
+    mp.value = (unsigned)(h->sweeps - g->sweeps0);
+    mp.elementSize = 4;
+    mp.width = 1;
+    mp.height = 1;
+    mp.pitch = 4;
+    CK(cudaGraphExecMemsetNodeSetParams(g->exec, g->off, &mp));
+  }
+  CK(cudaGraphLaunch(g->exec, h->stream));
+  g->used = ++h->graph_tick;
+  h->cur = g->cur2; h->prev = g->prev2; h->gen = g->gen2; h->gen_prev = g->gen_prev2; h->zmask = g->zmask2;
+  h->sweeps += g->n;
+  h->executed += g->n;
+  h->launches += g->launches;
+  return ABFT_OK;
+}
+
+// online (pipelined or serial) or unprotected sweeps of one slab, enqueued directly
+int run_direct(abft_stencil* h, int32_t n) {
+  if (h->cfg.mode == ABFT_MODE_ONLINE && h->pipe) return online_pipelined(h, n);
+  Group G{h};
+  for (int i = 0; i < n; ++i) TRY(h->cfg.mode == ABFT_MODE_ONLINE ? online_sweep(G) : none_sweep(G));
   return ABFT_OK;
 }
 
@@ -979,6 +1283,13 @@ int step_group(Group& G, int32_t n) {
     }
     return worst;
   }
+  if (G.size() == 1 && graph_eligible(G[0], n)) {
+    abft_stencil* h = G[0];
+    StepGraph* g = graph_find(h, n);
+    if (!g) TRY(graph_capture(h, n, &g));
+    return graph_launch(h, g);
+  }
+  if (mode == ABFT_MODE_ONLINE && G.size() == 1 && G[0]->pipe) return online_pipelined(G[0], n);
   for (int i = 0; i < n; ++i) TRY(mode == ABFT_MODE_ONLINE ? online_sweep(G) : none_sweep(G));
   return ABFT_OK;
 }
@@ -993,7 +1304,7 @@ struct IpcBlob {
   int64_t nx, ny, z_count, z_begin, plane, esz;
   cudaIpcMemHandle_t mem[4];   // field buffers 0..2, aux
   uint64_t off[4];
-  uint64_t off_gA[3], off_gB[3], off_PA[2], off_PB[2];
+  uint64_t off_gA[kGens], off_gB[kGens], off_PA[2], off_PB[2];
   cudaIpcEventHandle_t ev[2];
 };
 static_assert(sizeof(IpcBlob) <= ABFT_IPC_BLOB_BYTES, "blob size");
@@ -1086,6 +1397,16 @@ const char* abft_strerror(int s) {
   }
 }
 
+int abft_stencil_field_buffers(const abft_config* cfg, int32_t* n) {
+  if (!n) return ABFT_EINVAL;
+  const int v = validate(cfg);
+  if (v) return v;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return ABFT_ECUDA;
+  *n = (cfg->mode == ABFT_MODE_OFFLINE || k1_plan(cfg, dev).pipe) ? 3 : 2;
+  return ABFT_OK;
+}
+
 int abft_stencil_workspace_size(const abft_config* cfg, size_t* field_bytes, size_t* aux_bytes) {
   int v = validate(cfg);
   if (v) return v;
@@ -1108,7 +1429,12 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->cfg.points = h->points.data();
   h->cfg.sources = h->sources.data();
   h->L = layout(cfg);
-  h->nbuf = cfg->mode == ABFT_MODE_OFFLINE ? 3 : 2;
+  {
+    int dev0 = 0;
+    if (cudaGetDevice(&dev0) != cudaSuccess) { delete h; return ABFT_ECUDA; }
+    h->pipe = field_bufs[2] && k1_plan(cfg, dev0).pipe;
+  }
+  h->nbuf = (cfg->mode == ABFT_MODE_OFFLINE || h->pipe) ? 3 : 2;
   for (int b = 0; b < h->nbuf; ++b) {
     if (!field_bufs[b]) { delete h; return ABFT_EINVAL; }
     h->fb[b] = static_cast<char*>(field_bufs[b]);
@@ -1116,7 +1442,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->aux = static_cast<char*>(aux);
   h->stream = static_cast<cudaStream_t>(stream);
   const Layout& L = h->L;
-  for (int g = 0; g < 3; ++g) {
+  for (int g = 0; g < kGens; ++g) {
     h->gA[g] = reinterpret_cast<double*>(h->aux + L.off_gA[g]);
     h->gB[g] = reinterpret_cast<double*>(h->aux + L.off_gB[g]);
   }
@@ -1185,28 +1511,13 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
                   h->geo.tile_x + 2 * HV, h->geo.tile_y + 2))
       return fail(ABFT_ECUDA);
 
-  // launch geometry: z-chunks so the grid is >= ~8 waves of resident CTAs
+  // launch geometry and schedule (k1_plan)
   h->shape = match_shape(cfg);
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles_x = (int)((nx + h->geo.tile_x - 1) / h->geo.tile_x);
-  const int tiles_y = (int)((ny + h->geo.tile_y - 1) / h->geo.tile_y);
-  const int64_t tiles = (int64_t)tiles_x * tiles_y;
-  // z-chunks: ~32 waves of resident CTAs (the last, partial wave then costs
-  // little; measured on cfg4: 8 waves / 103 layers per CTA -> 32 waves / 28
-  // layers: protected K1 -3%), but >= 16 layers per CTA (each chunk re-stages
-  // its two z-halo layers)
-  const int per_sm = std::max(1, (228 * 1024) / (h->geo.smem + 1024));
-  const int64_t target = (int64_t)32 * nsm * per_sm;
-  int64_t nch = std::max<int64_t>(1, std::min<int64_t>(zc, (target + tiles - 1) / tiles));
-  int64_t zch = std::max<int64_t>((zc + nch - 1) / nch, std::min<int64_t>(zc, 16));
-  // ... unless that leaves SMs idle (few tiles and layers: cfg2), then about
-  // one wave
-  const int64_t slots = (int64_t)nsm * per_sm;
-  if (tiles * ((zc + zch - 1) / zch) < slots) zch = std::max<int64_t>(1, tiles * zc / slots);
-  h->zchunk = (int)zch;
-  if (const char* e = getenv("ABFT_ZCHUNK")) h->zchunk = std::max(1, std::min((int)zc, atoi(e)));
-  h->grid1 = dim3(tiles_x, tiles_y, (unsigned)((zc + h->zchunk - 1) / h->zchunk));
+  {
+    const K1Plan kp = k1_plan(cfg, dev);
+    h->zchunk = kp.zchunk;
+    h->grid1 = kp.grid;
+  }
 
   // parameter blocks (weights and coefficients rounded to the dtype)
   SweepParams& sp = h->sp;
@@ -1290,6 +1601,21 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
                       h->field_src, sp.coef, sp.scalar, h->cA, h->cB, h->stream) != cudaSuccess)
     return fail(ABFT_ECUDA);
   h->launches += 4;
+  h->zmask = ((1u << kGens) - 1) & ~1u;   // aux cleared, K0 wrote generation 0
+  if (const char* e = getenv("ABFT_GRAPHS")) h->graphs_on = atoi(e) != 0;
+  if (const char* e = getenv("ABFT_PIPE_PDL")) h->pipe_pdl = atoi(e) != 0;
+  if (h->pipe) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* pe = getenv("ABFT_S2_PRIO");   // experiment: 1 high, -1 low, 0 default
+    const int pv = pe ? atoi(pe) : 0;
+    const int prio = pv > 0 ? hi : (pv < 0 ? lo : 0);
+    if (cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, prio) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_k1, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_chk[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_chk[1], cudaEventDisableTiming) != cudaSuccess)
+      return fail(ABFT_ECUDA);
+  }
 
   // multi-GPU: NCCL communicator over NVLink, initial halo.  Without an id the
   // handle is a member of a local group (abft_stencil_group links them).
@@ -1383,13 +1709,13 @@ int abft_stencil_ipc_export(abft_stencil* h, void* blob) {
   IpcBlob b;
   memset(&b, 0, sizeof(b));
   b.magic = kIpcMagic;
-  b.version = 1;
+  b.version = 2;
   b.rank = h->cfg.rank; b.nranks = h->cfg.nranks; b.nbuf = h->nbuf;
   b.nx = h->cfg.nx; b.ny = h->cfg.ny; b.z_count = h->cfg.z_count; b.z_begin = h->cfg.z_begin;
   b.plane = h->L.plane; b.esz = h->L.esz;
   for (int k = 0; k < h->nbuf; ++k) TRY(ipc_handle(h->fb[k], &b.mem[k], &b.off[k]));
   TRY(ipc_handle(h->aux, &b.mem[3], &b.off[3]));
-  for (int g = 0; g < 3; ++g) { b.off_gA[g] = h->L.off_gA[g]; b.off_gB[g] = h->L.off_gB[g]; }
+  for (int g = 0; g < kGens; ++g) { b.off_gA[g] = h->L.off_gA[g]; b.off_gB[g] = h->L.off_gB[g]; }
   for (int g = 0; g < 2; ++g) { b.off_PA[g] = h->L.off_PA[g]; b.off_PB[g] = h->L.off_PB[g]; }
   for (int k = 0; k < 2; ++k) {
     if (!h->ev_ipc[k]) CK(cudaEventCreateWithFlags(&h->ev_ipc[k], cudaEventDisableTiming | cudaEventInterprocess));
@@ -1422,7 +1748,7 @@ int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_b
       h->proxy[1] = h->proxy[0];   // a ring of two ranks: one neighbour on both faces
       continue;
     }
-    if (b.magic != kIpcMagic || b.version != 1 || b.rank != want || b.nranks != h->cfg.nranks ||
+    if (b.magic != kIpcMagic || b.version != 2 || b.rank != want || b.nranks != h->cfg.nranks ||
         b.nx != h->cfg.nx || b.ny != h->cfg.ny || b.plane != h->L.plane || b.esz != h->L.esz ||
         b.nbuf != h->nbuf || b.z_begin != want_z) {
       r = ABFT_EINVAL;
@@ -1446,7 +1772,7 @@ int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_b
     if (r == ABFT_OK) r = ipc_open(h, seen, b.mem[3], &base);
     if (r != ABFT_OK) break;
     char* aux = base + b.off[3];
-    for (int g = 0; g < 3; ++g) {
+    for (int g = 0; g < kGens; ++g) {
       q->gA[g] = reinterpret_cast<double*>(aux + b.off_gA[g]);
       q->gB[g] = reinterpret_cast<double*>(aux + b.off_gB[g]);
     }
@@ -1503,6 +1829,14 @@ int abft_stencil_step(abft_stencil* h, int32_t n) {
   return step_group(G, n);
 }
 
+int abft_stencil_plan(abft_stencil* h, int32_t n) {
+  if (!h || n < 0 || h->grouped) return ABFT_EINVAL;
+  DevScope ds(h);
+  if (!graph_eligible(h, n) || graph_find(h, n)) return ABFT_OK;
+  StepGraph* g = nullptr;
+  return graph_capture(h, n, &g);
+}
+
 int abft_stencil_sweep(abft_stencil* h) {
   if (!h || h->grouped) return ABFT_EINVAL;
   DevScope ds(h);
@@ -1510,10 +1844,11 @@ int abft_stencil_sweep(abft_stencil* h) {
   Group G{h};
   if (h->cfg.mode == ABFT_MODE_NONE) return none_sweep(G);
   const int64_t s = h->sweeps + 1;
-  const int src = h->cur, dst = 1 - h->cur;
-  const int gn = (h->gen + 1) % 3;
+  const int src = h->cur, dst = next_buf(h);
+  const int gn = (h->gen + 1) % kGens;
   TRY(clear_summaries(h));
   TRY(zero_gen(h, gn));
+  h->zmask &= ~(1u << gn);
   TRY(launch_k1(h, src, dst, h->gA[gn], h->gB[gn], K1_CK_AB, s));
   TRY(halo_exchange(G, XSpec{dst, XV_GEN, gn}));
   h->prev = src;
@@ -1522,7 +1857,6 @@ int abft_stencil_sweep(abft_stencil* h) {
   h->gen = gn;
   h->sweeps = s;
   h->pending_check = true;
-  h->next_zero = false;
   return ABFT_OK;
 }
 
@@ -1619,7 +1953,8 @@ int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
   const int64_t nx = h->cfg.nx, ny = h->cfg.ny, zc = h->cfg.z_count;
   int g = h->gen, ga = h->gen;
   if (h->cfg.mode == ABFT_MODE_NONE) {  // no running checksums: compute them now (Eqs. 2-3)
-    g = ga = (h->gen + 1) % 3;
+    g = ga = (h->gen + 1) % kGens;
+    h->zmask &= ~(1u << g);
     if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,
                         h->gA[g], h->gB[g], 1, h->stream) != cudaSuccess)
       return ABFT_ECUDA;
@@ -1628,7 +1963,8 @@ int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
              !h->pending_check) {
     // lazy policy: a is not carried; compute it now into generation gen + 2
     // (cleared again by the next sweep's K2 before it is accumulated into)
-    ga = (h->gen + 2) % 3;
+    ga = (h->gen + 2) % kGens;
+    h->zmask &= ~(1u << ga);
     if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,
                         h->gA[ga], h->gB[ga], 1, h->stream) != cudaSuccess)
       return ABFT_ECUDA;
@@ -1721,6 +2057,11 @@ int abft_stencil_destroy(abft_stencil* h) {
   DevScope ds(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto e : h->ev) cudaEventDestroy(e);
+  if (h->s2) { cudaStreamSynchronize(h->s2); cudaStreamDestroy(h->s2); }
+  for (StepGraph& g : h->graphs) { cudaGraphExecDestroy(g.exec); cudaGraphDestroy(g.graph); }
+  if (h->cs) cudaStreamDestroy(h->cs);
+  for (cudaEvent_t e : {h->ev_k1, h->ev_chk[0], h->ev_chk[1]})
+    if (e) cudaEventDestroy(e);
   if (h->ev_ready) cudaEventDestroy(h->ev_ready);
   if (h->ev_pulled) cudaEventDestroy(h->ev_pulled);
   for (abft_stencil* q : h->members)   // unlink: the group is unusable once a member is gone

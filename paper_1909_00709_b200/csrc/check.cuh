@@ -132,9 +132,9 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
 // Eq. 1 for the one cell (z, y, x) of u^s from u^{s-1} (p.uprev), with the
 // ghosts of the boundary condition: the same canonical FMA chain as K1
 // (points in order, then the sources).  correction_form 2.
-template <typename T>
-__device__ T cell_update(const CheckParams& p, int z, int y, int x) {
-  const T* up = reinterpret_cast<const T*>(p.uprev);
+template <typename T, bool CG = false>
+__device__ T cell_update(const CheckParams& p, int z, int y, int x, const void* in = nullptr) {
+  const T* up = reinterpret_cast<const T*>(in ? in : p.uprev);
   const int nx = p.nx, ny = p.ny, zc = p.zc, bc = p.bc;
   const T g = bc == ABFT_BC_CONSTANT ? (T)p.g : T(0);
   T acc = T(0);
@@ -149,7 +149,8 @@ __device__ T cell_update(const CheckParams& p, int z, int y, int x) {
       const int bl = zmap(zz, zc, p.has_lo, p.has_hi, bc);
       const int yr = !yo ? yy : (bc == ABFT_BC_PERIODIC ? wrap(yy, ny) : max(0, min(yy, ny - 1)));
       const int xr = !xo ? xx : (bc == ABFT_BC_PERIODIC ? wrap(xx, nx) : max(0, min(xx, nx - 1)));
-      v = up[(size_t)bl * p.plane + (size_t)yr * p.px + xr];
+      const T* a = up + (size_t)bl * p.plane + (size_t)yr * p.px + xr;
+      v = CG ? __ldcg(a) : *a;
     }
     const T w = (T)p.w[q];
     acc = (q == 0) ? mul_rn(w, v) : fma_rn(w, v, acc);
@@ -166,6 +167,170 @@ __device__ T cell_update(const CheckParams& p, int z, int y, int x) {
 __device__ __forceinline__ bool same_bits(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
 __device__ __forceinline__ bool same_bits(double a, double b) {
   return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// ---------------------------------------------------------------- pipelined
+// Pipelined online schedule ("K2/K3 beside the next sweep"):
+// the checks of sweep s run while K1 of sweep s + 1 already reads u^s, so a
+// cell the checks rewrite may have been read before or after its repair.
+// Every rewrite is listed here; the CTA that finishes the check then waits for
+// that K1 and recomputes the cells of u^{s+1} whose stencil reads a rewritten
+// cell (fix_next), so u^{s+1} and its checksums end bitwise as if the checks
+// had run first -- the paper's order (fig.abft caption).
+__device__ __forceinline__ void note_change(const CheckParams& p, int z, int y, int x) {
+  if (!p.fix) return;
+  const int i = atomicAdd(&p.st->nchg, 1);
+  if (i < kChgCap) { p.st->chg[i][0] = z; p.st->chg[i][1] = y; p.st->chg[i][2] = x; }
+  atomicMax(&p.st->chg_zlo, 0x7fffffff - z);
+  atomicMax(&p.st->chg_zhi, z + 1);
+}
+
+// candidate d (0..26: offsets in {-1,0,1}^3) of rewritten cell c: the cell of
+// u^{s+1} at c + offset (periodic: wrapped; else outside -> false)
+__device__ __forceinline__ bool fix_cand(const CheckParams& p, const int* c, int d, int* o) {
+  const int off[3] = {d / 9 - 1, (d / 3) % 3 - 1, d % 3 - 1};
+  const int n[3] = {p.zc, p.ny, p.nx};
+  const bool per = p.bc == ABFT_BC_PERIODIC;
+  for (int a = 0; a < 3; ++a) {
+    int v = c[a] + off[a];
+    if (v < 0 || v >= n[a]) {
+      if (!per || (a == 0 && (p.has_lo || p.has_hi))) return false;
+      v = wrap(v, n[a]);
+    }
+    o[a] = v;
+  }
+  return true;
+}
+__device__ __forceinline__ bool near1(int a, int b, int n, bool per) {
+  const int d = abs(a - b);
+  return d <= 1 || (per && n - d <= 1);
+}
+
+// u^{s+1} at (z, y, x) recomputed from the repaired u^s (Eq. 1, the sweep's
+// FMA chain) with sweep s + 1's scheduled flips re-applied; stored and
+// the ledger patched if it differs.  Returns whether it changed.
+template <typename T>
+__device__ __forceinline__ bool fix_cell(const CheckParams& p, int z, int y, int x) {
+  T v = cell_update<T, true>(p, z, y, x, p.ucur);
+  for (int f = 0; f < p.nfn; ++f)
+    if (p.fn[f].z == z && p.fn[f].y == y && p.fn[f].x == x) v = flip_bit(v, p.fn[f].bit);
+  T* cell = reinterpret_cast<T*>(p.unext) + (size_t)(z + 1) * p.plane + (size_t)y * p.px + x;
+  if (same_bits(v, __ldcg(cell))) return false;
+  *cell = v;
+  if (p.EXnext) {
+    T* ex = reinterpret_cast<T*>(p.EXnext);
+    if (x == 0) ex[(size_t)(z + 1) * p.ny + y] = v;
+    if (x == p.nx - 1) ex[(size_t)(p.zc + 2) * p.ny + (size_t)(z + 1) * p.ny + y] = v;
+  }
+  return true;
+}
+// b^{s+1}[z][y] (and a^{s+1}[z][x]) re-summed from the fixed field: a sum over
+// values that now include no corrupted one is exact for fp32 data, so it
+// equals the atomic accumulation K1 would have made
+template <typename T>
+__device__ __forceinline__ void fix_row(const CheckParams& p, int z, int y) {
+  const T* row = reinterpret_cast<const T*>(p.unext) + (size_t)(z + 1) * p.plane + (size_t)y * p.px;
+  double b = 0.0;
+  for (int x = 0; x < p.nx; ++x) b += (double)__ldcg(row + x);
+  p.Bnext[(size_t)(z + 1) * p.ny + y] = b;
+}
+template <typename T>
+__device__ __forceinline__ void fix_col(const CheckParams& p, int z, int x) {
+  const T* col = reinterpret_cast<const T*>(p.unext) + (size_t)(z + 1) * p.plane + x;
+  double a = 0.0;
+  for (int y = 0; y < p.ny; ++y) a += (double)__ldcg(col + (size_t)y * p.px);
+  p.Anext[(size_t)(z + 1) * p.nx + x] = a;
+}
+
+// Run by every thread of the one CTA that finishes a pipelined check.
+template <typename T>
+__device__ __noinline__ void fix_next(const CheckParams& p) {
+  __shared__ int s_n, s_ok;
+  __shared__ unsigned s_chg[(kChgCap * 27 + 31) / 32];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_n = *(volatile int*)&p.st->nchg;
+    s_ok = 1;
+    if (s_n > 0 && p.fix) {   // wait for K1 of s + 1 (launched before this check could finish)
+      unsigned long long t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while (*(volatile unsigned*)&p.st->k1_cnt[(p.sweep + 1) & 1] < p.k1_target) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 4000000000ull) { s_ok = 0; break; }
+        __nanosleep(256);
+      }
+      __threadfence();
+    }
+  }
+  for (int i = tid; i < (kChgCap * 27 + 31) / 32; i += blockDim.x) s_chg[i] = 0u;
+  __syncthreads();
+  const int n = s_n;
+  if (n == 0) return;
+  const bool per = p.bc == ABFT_BC_PERIODIC;
+  if (!s_ok || !p.fix) {
+    if (tid == 0 && !s_ok) atomicMax(&p.st->worst, 3);   // K1 never finished: state unknown
+  } else if (n <= kChgCap) {
+    // the unique candidates: (i, d) is skipped when an earlier rewritten cell's
+    // neighbourhood or an earlier offset of the same cell reaches the same cell
+    const int m = n * 27;
+    for (int k = tid; k < m; k += blockDim.x) {
+      const int i = k / 27, d = k % 27;
+      const int* c = p.st->chg[i];
+      int o[3];
+      if (!fix_cand(p, c, d, o)) continue;
+      bool dup = false;
+      for (int j = 0; j < i && !dup; ++j)
+        dup = near1(o[0], p.st->chg[j][0], p.zc, per) && near1(o[1], p.st->chg[j][1], p.ny, per) &&
+              near1(o[2], p.st->chg[j][2], p.nx, per);
+      for (int e = 0; e < d && !dup; ++e) {
+        int q[3];
+        dup = fix_cand(p, c, e, q) && q[0] == o[0] && q[1] == o[1] && q[2] == o[2];
+      }
+      if (!dup && fix_cell<T>(p, o[0], o[1], o[2])) atomicOr(&s_chg[k / 32], 1u << (k % 32));
+    }
+    __syncthreads();
+    __threadfence_block();
+    // each row / column holding a changed cell, re-summed once (by its first changed candidate)
+    for (int k = tid; k < m; k += blockDim.x) {
+      if (!((s_chg[k / 32] >> (k % 32)) & 1u)) continue;
+      int o[3];
+      fix_cand(p, p.st->chg[k / 27], k % 27, o);
+      bool row_first = true, col_first = true;
+      for (int j = 0; j < k && (row_first || col_first); ++j) {
+        if (!((s_chg[j / 32] >> (j % 32)) & 1u)) continue;
+        int q[3];
+        fix_cand(p, p.st->chg[j / 27], j % 27, q);
+        if (q[0] == o[0] && q[1] == o[1]) row_first = false;
+        if (q[0] == o[0] && q[2] == o[2]) col_first = false;
+      }
+      if (row_first) fix_row<T>(p, o[0], o[1]);
+      if (col_first && p.Anext) fix_col<T>(p, o[0], o[2]);
+    }
+  } else {
+    // many rewrites (a layer recompute, Q27): every cell of the layers within
+    // one of a rewritten layer, then all their rows and columns.  Rare, slow.
+    const int zlo = 0x7fffffff - *(volatile int*)&p.st->chg_zlo, zhi = *(volatile int*)&p.st->chg_zhi - 1;
+    auto member = [&](int z) {
+      if (z >= zlo - 1 && z <= zhi + 1) return true;
+      if (!per || p.has_lo || p.has_hi) return false;
+      return (zlo == 0 && z == p.zc - 1) || (zhi == p.zc - 1 && z == 0);
+    };
+    const int64_t lay = (int64_t)p.ny * p.nx;
+    for (int z = 0; z < p.zc; ++z) {
+      if (!member(z)) continue;
+      for (int64_t e = tid; e < lay; e += blockDim.x) fix_cell<T>(p, z, (int)(e / p.nx), (int)(e % p.nx));
+    }
+    __syncthreads();
+    __threadfence_block();
+    for (int z = 0; z < p.zc; ++z) {
+      if (!member(z)) continue;
+      for (int y = tid; y < p.ny; y += blockDim.x) fix_row<T>(p, z, y);
+      if (p.Anext)
+        for (int x = tid; x < p.nx; x += blockDim.x) fix_col<T>(p, z, x);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) { p.st->nchg = 0; p.st->chg_zlo = 0; p.st->chg_zhi = 0; }
 }
 
 // correction_form 2 when the flags of layer z do not intersect in one cell
@@ -189,6 +354,7 @@ __device__ __noinline__ void recompute_layer(const CheckParams& p, int z, abft_r
       const T v = cell_update<T>(p, z, y, x), uo = *cell;
       if (!same_bits(v, uo)) {
         *cell = v;
+        note_change(p, z, y, x);
         for (int f = 0; f < 2; ++f)   // fused halo: the neighbour's copy
           if (z == (f == 0 ? 0 : zc - 1) && p.peerU[f])
             reinterpret_cast<T*>(p.peerU[f])[(size_t)y * p.px + x] = v;
@@ -239,7 +405,7 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
   const int tid = threadIdx.x, bz = z + 1, nx = p.nx, ny = p.ny, zc = p.zc;
   if ((na | nb) == 0) return;
   abft_record r;
-  r.sweep = p.sweep; r.z = p.z_begin + z; r.y = y0; r.x = x0;
+  r.sweep = p.sweep + *(volatile int*)&p.st->sweep_off; r.z = p.z_begin + z; r.y = y0; r.x = x0;
   r.observed = 0.0; r.corrected = 0.0; r.vx = 0.0; r.vy = 0.0;
   r.nflag_a = na; r.nflag_b = nb; r.pad = 0;
   if (p.flags & CK_OFFLINE_END) {
@@ -290,6 +456,7 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
         *by += (double)cor - uo;
       }
       *cell = cor;
+      note_change(p, z, y0, x0);
       for (int f = 0; f < 2; ++f) {   // fused halo: the neighbours' copies
         if (z != (f == 0 ? 0 : zc - 1)) continue;
         if (p.peerU[f]) reinterpret_cast<T*>(p.peerU[f])[(size_t)y0 * p.px + x0] = cor;
@@ -386,7 +553,7 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
   }
 }
 template <typename T, int S, bool BCG>
-__global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
+__device__ __forceinline__ void k2_layer(const CheckParams& p) {
   const int z = p.zr0 + blockIdx.x, bz = z + 1;
   const int tid = threadIdx.x, part = blockIdx.y, nparts = gridDim.y;
   LayerSummary* L = &p.summ[z];
@@ -397,6 +564,7 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   double pa, pb;
   (void)bz;
   grid_dependency_wait();   // K1's checksums and field (PDL)
+  if (p.k1_reset && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) p.st->k1_cnt[p.sweep & 1] = 0u;
   if (!(p.flags & CK_FROM_SUMMARY)) {
     if (tid == 0) { s_na = 0; s_nb = 0; s_xk = 0; s_yk = 0; s_pa = 0.0; s_pb = 0.0; }
     __syncthreads();
@@ -473,6 +641,24 @@ __global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant_
   const int x0 = na ? 0x7fffffff - xk : -1;
   const int y0 = nb ? 0x7fffffff - yk : -1;
   finish_layer<T>(p, z, na, nb, x0, y0, pa, pb, red);
+}
+template <typename T, int S, bool BCG>
+__global__ void __launch_bounds__(kCheckThreads) k2_check(const __grid_constant__ CheckParams p) {
+  k2_layer<T, S, BCG>(p);
+  if (p.fix && !(p.flags & CK_LAZY)) {
+    // pipelined schedule, policy BOTH: the CTA that finishes K2 last repairs
+    // u^{s+1} where K1 of s + 1 read a cell this check rewrote
+    __shared__ int s_fin;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_fin = atomicAdd(&p.st->k2_done, 1) == (int)(gridDim.x * gridDim.y) - 1;
+    __syncthreads();
+    if (s_fin) {
+      __threadfence();
+      fix_next<T>(p);
+      if (threadIdx.x == 0) p.st->k2_done = 0;
+    }
+  }
 }
 
 // K3 (lazy checksum policy): for the layers whose b flagged in K2, the
@@ -558,6 +744,7 @@ __global__ void __launch_bounds__(kCheckThreads) k3_lazy(const __grid_constant__
     p.lazy_mark[(e >> 30) * (zc + 2) + (e & 0x3fffffff)] = 0;
   }
   if (tid == 0) p.st->lazy_done = 0;
+  if (p.fix) fix_next<T>(p);   // pipelined schedule (see fix_next)
 }
 
 // ---------------------------------------------------------------- K0

@@ -16,6 +16,8 @@ constexpr int kMaxSources = 4;
 constexpr int kMaxFaultsPerLaunch = 64;   // scheduled flips per sweep and slab (set_faults checks)
 constexpr int kRecordCap = 4096;
 constexpr int kMaxDevices = 64;          // per-device launch attributes
+constexpr int kGens = 4;                 // rotating checksum generations (pipelined schedule: 4)
+constexpr int kChgCap = 32;              // pipelined schedule: changed cells listed per sweep
 
 // ------------------------------------------------------------------ shapes
 // The sweep evaluates the points of S in the caller's order (the FMA chain is
@@ -96,6 +98,14 @@ struct DevState {
   int lazy_n[2];             // lazy checksum policy: layers whose b flagged, by sweep parity
   int lazy_rows[2];          // lazy policy: a rows to compute, by sweep parity
   int lazy_done;             // lazy policy: K3 CTAs finished
+  // pipelined online schedule (K2/K3 of sweep s beside K1 of sweep s + 1):
+  // the cells of u^s the checks rewrote (the first kChgCap of nchg), the
+  // extent of their layers, K1 CTAs completed (monotonic), K2 CTAs done
+  int nchg, chg_zlo, chg_zhi, k2_done;
+  unsigned k1_cnt[2];        // K1 CTAs finished, by sweep parity (K2 of that sweep resets it)
+  int sweep_off;             // added to the recorded sweep (a cached graph replayed later)
+  int pad_;
+  int chg[kChgCap][3];       // (z, y, x), slab-local
   abft_record rec[kRecordCap];
 };
 enum { ST_SWEEPS = 0, ST_DETECT, ST_LOCATED, ST_CORRECTED, ST_UNLOCATED, ST_UNCORR,
@@ -162,6 +172,19 @@ struct CheckParams {
   int flags, form;
   long long sweep, z_begin;
   int zr0, zr1;        // slab-local layers of this launch, [zr0, zr1) (K2: one per grid.x)
+  // pipelined schedule: K1 of sweep s + 1 ran beside this check reading u^s
+  // (ucur) while it was corrected; the kernel that finishes the check (K2
+  // under BOTH, K3 under LAZY) waits for it (k1_cnt[(s + 1) & 1] == k1_target) and
+  // recomputes the cells of u^{s+1} that read a rewritten cell (fix_next)
+  int fix;             // 1: K1 of s + 1 is in flight; 0: only list / clear
+  int nfn;             // flips of sweep s + 1 in this slab (re-applied by the fix)
+  unsigned k1_target;  // CTAs of K1 of s + 1 (DevState::k1_cnt[(s + 1) & 1] when it is done)
+  int k1_reset;        // pipelined: K2 clears DevState::k1_cnt[s & 1] (K1 of s is done)
+  void* unext;         // u^{s+1} buffer
+  double* Anext;       // a^{s+1} (null under LAZY), b^{s+1}
+  double* Bnext;
+  void* EXnext;        // edge columns of u^{s+1}
+  LocalFault fn[kMaxFaultsPerLaunch];
 };
 
 struct SweepParams {
@@ -190,6 +213,7 @@ struct SweepParams {
   const void* src;               // that field, [zc][ny][spx] (16-byte aligned rows)
   int64_t spx, splane;
   void* EX;            // edge columns of the output: [2][zc+2][ny] (x = 0, x = nx-1), or null
+  unsigned* done;      // pipelined schedule: +1 per finished CTA (DevState::k1_cnt), or null
   int nfaults;
   LocalFault faults[kMaxFaultsPerLaunch];
 };

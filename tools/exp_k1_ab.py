@@ -19,18 +19,20 @@ for name in libs:
 p = make_problem("cfg4")
 dev = torch.device("cuda:0")
 u0, P = field_u0(p, dev), field_power(p, dev)
-res = {n: {"none": [], "lazy": [], "both": []} for n in libs}
+res = {n: {"none": [], "lazy": [], "both": [], "k2_lazy": [], "k2_both": []} for n in libs}
 for rep in range(reps):
     for name in libs:
         abft._lib = None
         abft.LIB_PATH = handles[name]
         for tag, mode, pol in (("none", 0, 0), ("lazy", 1, 1), ("both", 1, 0)):
-            st = abft.from_problem(p, u0, P, device=dev, mode=mode, checksum_policy=pol)
+            st = abft.from_problem(p, u0, P, device=dev, mode=mode, checksum_policy=pol, schedule=1)
             st.step(3)
             st.profile(True)
             st.step(10)
             r = st.profile_read()
             res[name][tag].append(r["k1_ms"] / r["k1_launches"])
+            if tag != "none":
+                res[name]["k2_" + tag].append(r["k2_ms"] / 10)
             st.destroy()
 out = {n: {t: round(statistics.median(v), 5) for t, v in d.items()} for n, d in res.items()}
 for n, d in out.items():
