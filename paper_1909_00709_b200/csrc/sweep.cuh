@@ -700,17 +700,24 @@ __global__ void __launch_bounds__(Tile<T>::THREADS, 256 / Tile<T>::THREADS * ABF
       }
     }
     // ledger for Theorem 1's beta terms of the next check: the x-edge columns
+    // (only the lane holding column 0 or nx - 1 branches in: a per-cell
+    // compare in every lane of an edge tile cost ~1 ISETP per cell)
     if (exl && xedge) {
       const size_t lay = (size_t)(z + 1) * ny;
-      const size_t side = (size_t)(zc + 2) * ny;
+      const int kr = nx - 1 - gx0;   // column nx - 1 in this thread's vector?
+      if (gx0 == 0) {
 #pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        const int gy = gyb + r;
-        if (gy >= ny) continue;
+        for (int r = 0; r < RY; ++r)
+          if (gyb + r < ny) exl[lay + gyb + r] = out[r][0];
+      }
+      if (kr >= 0 && kr < V) {
+        T* exr = exl + (size_t)(zc + 2) * ny + lay + gyb;
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-          if (gx0 + k == 0) exl[lay + gy] = out[r][k];
-          if (gx0 + k == nx - 1) exl[side + lay + gy] = out[r][k];
+        for (int r = 0; r < RY; ++r) {
+          T v = out[r][0];
+#pragma unroll
+          for (int k = 1; k < V; ++k) v = k == kr ? out[r][k] : v;
+          if (gyb + r < ny) exr[r] = v;
         }
       }
     }
