@@ -392,10 +392,13 @@ def run_ours(a):
             "config": {"workload": f"{a.config}: {stencil_name(p)} {p.nx}x{p.ny}x{p.nz} "
                                    f"{p.dtype}, {'online' if pmode == 1 else 'offline (period %d)' % p.delta}"
                                    f" ABFT, {K} sweeps, {len(faults)} scheduled bit-flips",
-                       "checksum_policy": ("offline windows: a and b at each window end" if pmode == 2 else
+                       "checksum_policy": ("lazy offline: b alone predicted every sweep, summed and compared at "
+                                           "each window end (no correction offline, so a is never needed; "
+                                           "PAPER.md:271-273, 496-497; DESIGN.md Q29)" if pmode == 2 else
                                            "lazy: b every sweep, a for layers whose b flags "
                                            "(PAPER.md:271-273, 496-497)") if pol == abft.ABFT_CK_LAZY
-                       else "both: a and b every sweep in the K1 pass",
+                       else ("both offline: a and b at each window end" if pmode == 2 else
+                             "both: a and b every sweep in the K1 pass"),
                        "nx": p.nx, "ny": p.ny, "nz": p.nz, "z_per_gpu": zc,
                        "parallelism": (f"z-slab x{world} ({'CUDA IPC fused halo' if transport == 'ipc' else 'NCCL halo'})"
                                        if world > 1 else "1 GPU"),

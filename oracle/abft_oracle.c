@@ -505,8 +505,10 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
         int64_t dirty = 0, zmin = nz, zmax = -1;
         for (int64_t z = zlo; z <= zhi; z++) {
           int64_t na = 0, nb = 0, x0 = -1, y0 = -1;
-          for (int64_t x = 0; x < nx; x++)
-            if (or_flag(PA[z * nx + x], An[z * nx + x], p->eps)) { if (x0 < 0) x0 = x; na++; }
+          /* checksums 1 (Q29): detection by b alone -- a is never compared */
+          if (p->checksums != 1)
+            for (int64_t x = 0; x < nx; x++)
+              if (or_flag(PA[z * nx + x], An[z * nx + x], p->eps)) { if (x0 < 0) x0 = x; na++; }
           for (int64_t y = 0; y < ny; y++)
             if (or_flag(PB[z * ny + y], Bn[z * ny + y], p->eps)) { if (y0 < 0) y0 = y; nb++; }
           if (na + nb == 0) continue;

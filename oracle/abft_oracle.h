@@ -63,7 +63,11 @@ typedef struct {
                               2 recompute the located cell from u^(t) */
   int32_t checksums;   /* online: 0 = a and b every sweep (SURVEY Q8 reading);
                           1 = b every sweep, a only for layers whose b flags
-                          (the paper's recommendation) */
+                          (the paper's recommendation);
+                          offline: 0 = a and b compared at each window end,
+                          1 = b only (offline never corrects, so the second
+                          vector the paper computes "to enable correction" is
+                          never needed; Q29) */
   int32_t recovery;    /* offline, dirty window: 0 = roll back to the window's
                           checkpoint and re-execute it;
                           1 = re-execute only the layers an error detected in

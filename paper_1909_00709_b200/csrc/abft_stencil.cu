@@ -1008,15 +1008,17 @@ int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, 
       const double* pA = k == 1 ? h->gA[ckgen] : h->PA[(k - 1) & 1];
       const double* pB = k == 1 ? h->gB[ckgen] : h->PB[(k - 1) & 1];
       CheckParams c;
+      const bool bonly = h->cfg.checksum_policy == ABFT_CK_LAZY;   // Q29
       if (!end) {
         TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s, za, zb));
         c = make_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[k & 1], h->PB[k & 1], nullptr,
-                       nullptr, CK_STORE_PRED, s);
+                       nullptr, CK_STORE_PRED | (bonly ? CK_BONLY : 0), s);
       } else {
         TRY(zero_gen(h, gend, za, zb));
-        TRY(launch_k1(h, src, dst, h->gA[gend], h->gB[gend], K1_CK_AB, s, za, zb));
+        TRY(launch_k1(h, src, dst, bonly ? nullptr : h->gA[gend], h->gB[gend], bonly ? K1_CK_B : K1_CK_AB, s,
+                      za, zb));
         c = make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
-                       nullptr, CK_COMPARE | CK_OFFLINE_END | CK_PERSIST, s);
+                       nullptr, CK_COMPARE | CK_OFFLINE_END | CK_PERSIST | (bonly ? CK_BONLY : 0), s);
       }
       c.zr0 = za;
       c.zr1 = zb;
@@ -1062,17 +1064,20 @@ int offline_window(Group& G, int L) {
         for (abft_stencil* h : G) {
           const double* pA = t == 1 ? h->gA[ckgen] : h->PA[(t - 1) & 1];
           const double* pB = t == 1 ? h->gB[ckgen] : h->PB[(t - 1) & 1];
+          // policy LAZY offline (Q29): b predicted, summed and compared alone
+          const bool bonly = h->cfg.checksum_policy == ABFT_CK_LAZY;
+          const int bf = bonly ? CK_BONLY : 0;
           if (!end) {
             TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
             TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
-                             nullptr, nullptr, CK_STORE_PRED, s));
+                             nullptr, nullptr, CK_STORE_PRED | bf, s));
           } else {
             TRY(zero_gen(h, gend));
-            TRY(sweep_checked(h, src, dst, h->gA[gend], h->gB[gend],
-                              make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr,
-                                         nullptr, nullptr, nullptr,
-                                         CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0), s),
-                              s));
+            TRY(launch_k1(h, src, dst, bonly ? nullptr : h->gA[gend], h->gB[gend], bonly ? K1_CK_B : K1_CK_AB,
+                          s));
+            TRY(launch_check(h, make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr,
+                                           nullptr, nullptr,
+                                           CK_COMPARE | CK_OFFLINE_END | (attempt ? CK_PERSIST : 0) | bf, s)));
           }
         }
         TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, t & 1}));
@@ -1959,10 +1964,11 @@ int abft_stencil_checksums(abft_stencil* h, double* A, double* B) {
                         h->gA[g], h->gB[g], 1, h->stream) != cudaSuccess)
       return ABFT_ECUDA;
     h->launches += 2;
-  } else if (h->cfg.mode == ABFT_MODE_ONLINE && h->cfg.checksum_policy == ABFT_CK_LAZY &&
-             !h->pending_check) {
-    // lazy policy: a is not carried; compute it now into generation gen + 2
-    // (cleared again by the next sweep's K2 before it is accumulated into)
+  } else if (h->cfg.checksum_policy == ABFT_CK_LAZY &&
+             ((h->cfg.mode == ABFT_MODE_ONLINE && !h->pending_check) || h->cfg.mode == ABFT_MODE_OFFLINE)) {
+    // lazy policy: a is not carried (online: K3 computes it for flagged
+    // layers only; offline: never, Q29); compute it now into generation
+    // gen + 2 (cleared again before it is accumulated into)
     ga = (h->gen + 2) % kGens;
     h->zmask &= ~(1u << ga);
     if (launch_k0_field(h->cfg.dtype, h->fb[h->cur], h->L.px, h->L.plane, (int)nx, (int)ny, (int)zc,

@@ -572,7 +572,9 @@ __device__ __forceinline__ void k2_layer(const CheckParams& p) {
     // round, so the loads of all kCheckUnroll entries are in flight together.
     // Lazy policy: b' only; a is computed by K3 for the
     // layers whose b flags.  nparts > 1 (few layers): this CTA's share.
-    if (!(p.flags & CK_LAZY)) check_vec<T, S, true, BCG>(p, z, &s_na, &s_xk, &s_pa, part, nparts);
+    // Offline under LAZY (CK_BONLY, Q29): b' only, and no K3 -- a window
+    // is rolled back, never corrected, so a is never needed.
+    if (!(p.flags & (CK_LAZY | CK_BONLY))) check_vec<T, S, true, BCG>(p, z, &s_na, &s_xk, &s_pa, part, nparts);
     check_vec<T, S, false, BCG>(p, z, &s_nb, &s_yk, &s_pb, part, nparts);
     if (!(p.flags & CK_COMPARE)) return;
     __syncthreads();

@@ -130,6 +130,7 @@ enum CheckFlags {
   CK_SUMMARY = 32,       // write LayerSummary (explicit check())
   CK_FROM_SUMMARY = 64,  // correct() from a stored summary, no prediction
   CK_LAZY = 128,         // checksum policy LAZY: compare b only; flagged layers -> K3
+  CK_BONLY = 256,        // offline, policy LAZY: predict / compare b only (Q29)
 };
 
 struct CheckParams {

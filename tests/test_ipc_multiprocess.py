@@ -89,6 +89,11 @@ CASES = {
     "lazy": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=1, checksums=1),
     "offline": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=28, nfaults=8, mode=2, delta=7),
     "partial": dict(name="cfg3", nx=96, ny=80, nz=24, sweeps=18, mode=2, delta=6, recovery=1),
+    # offline under policy LAZY: b alone predicted, summed, compared (Q29)
+    "offline_lazy": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=28, nfaults=8, mode=2, delta=7,
+                         checksums=1),
+    "partial_lazy": dict(name="cfg3", nx=96, ny=80, nz=24, sweeps=18, mode=2, delta=6, recovery=1,
+                         checksums=1),
     "periodic": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=1, bc=1),
     "periodic_offline": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=20, nfaults=6, mode=2, delta=5,
                              bc=1, recovery=1),
@@ -100,7 +105,7 @@ CASES = {
 def test_ipc_processes_equal_oracle(world, case):
     pkw = CASES[case]
     p = make_problem(pkw["name"], **{k: v for k, v in pkw.items() if k != "name"})
-    if case == "partial":
+    if case.startswith("partial"):
         faults = [Fault(1, 11, 7, 9, 24), Fault(7, 0, 79, 95, 30), Fault(13, 23, 0, 0, 28),
                   Fault(13, 5, 5, 5, 29)]
     else:

@@ -634,3 +634,78 @@ def test_partial_reexecution_keeps_layers_no_detected_error_reached():
     assert (full["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
     assert (part["u"].view(np.uint32) == only_lo["u"].view(np.uint32)).all()
     assert not (part["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+
+
+# ------------------------------- offline, detection by b alone (Q29)
+
+@pytest.mark.parametrize("checksums", [0, 1])
+def test_offline_window_detection_closed_form(checksums):
+    # Offline windows of one sweep (Delta = 1), one flip at sweep s: the
+    # prediction is Theorem 1 applied to the verified checksums of u^{s-1}
+    # (the clean row / column sums up to ~1e-8), the actual window-end sums
+    # differ from the clean ones by exactly d = flipped - clean.  So b[y]
+    # flags iff |d| > eps |S_row + d| and a[x] iff |d| > eps |S_col + d|.
+    # checksums = 1 (one vector compared, the second computed only
+    # "to enable correction" -- which offline never does): a window is dirty
+    # iff b flags, its record has nflag_a = 0 and x = -1; both policies roll
+    # the window back, so the result is the fault-free run.
+    p = _cfg1_like().replace(mode=2, delta=1, checksums=checksums)
+    op = O.OProblem(p)
+    u0 = field_u0(p).numpy()
+    s = 10
+    clean = _clean_states(p, op, u0, s)
+    ref = O.run(op, u0, s)
+    rng = random.Random(29)
+    checked = 0
+    for trial in range(80):
+        y, x, bit = rng.randrange(64), rng.randrange(64), rng.randrange(31)
+        cv = np.array([clean[0, y, x]], np.float32)
+        fv = cv.copy()
+        O.flip(fv, 0, bit)
+        d = float(fv[0]) - float(cv[0])
+        Srow = math.fsum(float(v) for v in clean[0, y, :])
+        Scol = math.fsum(float(v) for v in clean[0, :, x])
+        mb = abs(d) / abs(Srow + d) if math.isfinite(d) else math.inf
+        ma = abs(d) / abs(Scol + d) if math.isfinite(d) else math.inf
+        if 0.9 * p.eps < mb < 1.1 * p.eps or 0.9 * p.eps < ma < 1.1 * p.eps:
+            continue                               # ambiguous band
+        r = O.run(op, u0, s, [Fault(s, 0, y, x, bit)])
+        expect_b, expect_a = mb > p.eps, ma > p.eps
+        dirty = expect_b if checksums == 1 else (expect_a or expect_b)
+        first = [q for q in r["records"] if q["status"] == O.REC_WINDOW_DIRTY]
+        assert r["stats"]["rollbacks"] == int(dirty) and r["status"] == 0
+        if dirty:
+            (rec,) = first
+            assert rec["sweep"] == s and rec["z"] == 0
+            assert rec["nflag_b"] == int(expect_b) and rec["y"] == (y if expect_b else -1)
+            assert rec["nflag_a"] == (0 if checksums == 1 else int(expect_a))
+            assert rec["x"] == (x if (expect_a and checksums == 0) else -1)
+            assert (r["u"].view(np.uint32) == ref["u"].view(np.uint32)).all()
+        else:
+            assert first == []
+        checked += 1
+    assert checked > 50
+
+
+def test_offline_b_only_equals_both_when_b_flags():
+    # every flip large enough to flag its b entry (bits 24-30 of values in
+    # [323, 343)): comparing b alone rolls back exactly the windows BOTH
+    # rolls back, so the field and the checksums are bitwise BOTH's -- the
+    # fault-free run -- and the records differ only in the a fields
+    p = make_problem("cfg3", nx=40, ny=32, nz=8, sweeps=20, mode=2, delta=5)
+    P = field_power(p).numpy()
+    u0 = field_u0(p).numpy()
+    rng = random.Random(31)
+    faults = [Fault(s, rng.randrange(8), rng.randrange(32), rng.randrange(40), rng.randint(24, 30))
+              for s in (2, 5, 9, 13, 14, 18)]
+    both = O.run(O.OProblem(p, [P]), u0, p.sweeps, faults)
+    bonly = O.run(O.OProblem(p.replace(checksums=1), [P]), u0, p.sweeps, faults)
+    clean = O.run(O.OProblem(p, [P]), u0, p.sweeps)
+    assert both["stats"]["rollbacks"] == 4 and bonly["stats"] == both["stats"]
+    for r in (both, bonly):
+        assert (r["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+        assert np.array_equal(r["A"], clean["A"]) and np.array_equal(r["B"], clean["B"])
+    strip = lambda q: {k: v for k, v in q.items() if k not in ("nflag_a", "x")}
+    assert [strip(q) for q in bonly["records"]] == [strip(q) for q in both["records"]]
+    assert all(q["nflag_a"] == 0 and q["x"] == -1 for q in bonly["records"])
+    assert all(q["nflag_b"] >= 1 for q in bonly["records"])
