@@ -112,15 +112,29 @@ cudaError_t prime_checks(int dtype, int shape, int bc) {
   return cudaGetLastError();
 }
 
+// K0 launches: column sums (a thread per 16-byte vector of columns) and row
+// sums (a warp per 32 rows, 8 warps per CTA), each in ascending index order
+template <typename F, typename E, typename T>
+static void k0_pair(const F& f, int nx, int ny, int zc, double* A, double* B, int off, cudaStream_t s) {
+  constexpr int V = 16 / (int)sizeof(T);
+  const unsigned cb = (unsigned)((int64_t)zc * ((nx + 256 * V - 1) / (256 * V)));
+  k0_colsum<F, E, T><<<cb, 256, 0, s>>>(f, nx, ny, A, off);
+  const unsigned rb = (unsigned)(((int64_t)zc * ny + 255) / 256);
+  k0_rowsum<F, E, T><<<rb, 256, 0, s>>>(f, nx, ny, zc, B, off);
+}
+
 cudaError_t launch_k0_field(int dtype, const void* u, int64_t px, int64_t plane, int nx, int ny,
                             int zc, double* A, double* B, int off, cudaStream_t s) {
   FieldVal f{u, px, plane, dtype};
-  const int V = dtype == ABFT_F32 ? 4 : 2;
-  const unsigned cb = (unsigned)((int64_t)zc * ((nx + 256 * V - 1) / (256 * V)));
-  if (dtype == ABFT_F32) k0_colsum<FieldVal, float><<<cb, 256, 0, s>>>(f, nx, ny, A, off);
-  else k0_colsum<FieldVal, double><<<cb, 256, 0, s>>>(f, nx, ny, A, off);
-  k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, B, off);
+  if (dtype == ABFT_F32) k0_pair<FieldVal, FieldEval, float>(f, nx, ny, zc, A, B, off, s);
+  else k0_pair<FieldVal, FieldEval, double>(f, nx, ny, zc, A, B, off, s);
   return cudaGetLastError();
+}
+
+template <int NPOST>
+static void k0_const_go(const ConstVal& f, int nx, int ny, int zc, double* A, double* B, cudaStream_t s) {
+  if (f.dtype == ABFT_F32) k0_pair<ConstVal, ConstEval<NPOST>, float>(f, nx, ny, zc, A, B, 0, s);
+  else k0_pair<ConstVal, ConstEval<NPOST>, double>(f, nx, ny, zc, A, B, 0, s);
 }
 
 cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, int ny, int zc,
@@ -133,11 +147,14 @@ cudaError_t launch_k0_const(int dtype, const void* field, int64_t fpx, int nx, i
     f.coef[q] = q < nsources ? coef[q] : 0.0;
     f.scalar[q] = q < nsources ? scalar[q] : 0.0;
   }
-  const int V = dtype == ABFT_F32 ? 4 : 2;
-  const unsigned cb = (unsigned)((int64_t)zc * ((nx + 256 * V - 1) / (256 * V)));
-  if (dtype == ABFT_F32) k0_colsum<ConstVal, float><<<cb, 256, 0, s>>>(f, nx, ny, cA, 0);
-  else k0_colsum<ConstVal, double><<<cb, 256, 0, s>>>(f, nx, ny, cA, 0);
-  k0_rowsum<<<(unsigned)(((int64_t)zc * ny + 255) / 256), 256, 0, s>>>(f, dtype, nx, ny, zc, cB, 0);
+  // constant terms after the field term (none without a field source)
+  const int npost = field_src >= 0 ? nsources - field_src - 1 : 0;
+  switch (npost) {
+    case 0: k0_const_go<0>(f, nx, ny, zc, cA, cB, s); break;
+    case 1: k0_const_go<1>(f, nx, ny, zc, cA, cB, s); break;
+    case 2: k0_const_go<2>(f, nx, ny, zc, cA, cB, s); break;
+    default: k0_const_go<3>(f, nx, ny, zc, cA, cB, s); break;
+  }
   return cudaGetLastError();
 }
 
