@@ -129,6 +129,104 @@ __device__ __forceinline__ double predict_entry(const CheckParams& p, int z, int
   return acc;
 }
 
+// The layer-uniform part of the prediction of layer z (the same for every
+// entry a CTA predicts, computed once per CTA instead of once per point and
+// entry): per plane offset dk = d - 1 the predictor row of layer zeta(z + dk),
+// whether that layer is a zero / constant ghost, the layer of u^{s-1} (alpha:
+// its top / bottom rows; beta without a ledger: its edge columns) and the
+// x-edge ledger rows of u^{s-1} (beta).
+template <typename T, bool A>
+struct PredLayer {
+  const double* prow[3];
+  const T* lay[3];
+  const T* exl[3];
+  const T* exr[3];
+  bool zg[3];
+  const double* crow;
+};
+template <typename T, bool A, bool BCG>
+__device__ __forceinline__ PredLayer<T, A> pred_layer(const CheckParams& p, int z) {
+  PredLayer<T, A> L;
+  const int bc = BCG ? p.bc : ABFT_BC_CLAMP;
+  const T* up = reinterpret_cast<const T*>(p.uprev);
+  const T* ex = reinterpret_cast<const T*>(p.EXp);
+  const size_t side = (size_t)(p.zc + 2) * p.ny;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int zq = zmap(z + d - 1, p.zc, p.has_lo, p.has_hi, bc);
+    L.zg[d] = zghost(z + d - 1, p.zc, p.has_lo, p.has_hi, bc);
+    L.prow[d] = A ? p.Ap + (size_t)zq * p.nx : p.Bp + (size_t)zq * p.ny;
+    L.lay[d] = up + (size_t)zq * p.plane;
+    const bool led = !A && ex && zq >= 1 && zq <= p.zc;
+    L.exl[d] = led ? ex + (size_t)zq * p.ny : nullptr;
+    L.exr[d] = led ? ex + side + (size_t)zq * p.ny : nullptr;
+  }
+  L.crow = A ? p.cA + (size_t)z * p.nx : p.cB + (size_t)z * p.ny;
+  return L;
+}
+// predict_entry for a compile-time point list with the layer part hoisted:
+// the same operations in the same order, so the same bits
+template <typename T, int S, bool A, bool BCG>
+__device__ __forceinline__ double predict_entry_l(const CheckParams& p, const PredLayer<T, A>& L, int e) {
+  using SH = Shape<S>;
+  constexpr int NP = SH::NP;
+  const int nx = p.nx, ny = p.ny;
+  const int bc = BCG ? p.bc : ABFT_BC_CLAMP;
+  const bool ghostv = bc == ABFT_BC_ZERO || bc == ABFT_BC_CONSTANT;
+  const double g = bc == ABFT_BC_CONSTANT ? p.g : 0.0;
+  double Sv[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int di = SH::off(q, 0), dj = SH::off(q, 1), d = SH::off(q, 2) + 1;
+    if (A) {
+      const int xs = e + di;
+      const bool xg = ghostv && (xs < 0 || xs >= nx);
+      if (L.zg[d] || xg) {
+        Sv[q] = __dmul_rn((double)ny, g);
+        continue;
+      }
+      const int xr = (xs >= 0 && xs < nx) ? xs : (bc == ABFT_BC_PERIODIC ? wrap(xs, nx) : max(0, min(xs, nx - 1)));
+      double s = L.prow[d][xr];
+      if (dj != 0) {   // alpha at the shifted column (Q3)
+        const T* col = L.lay[d] + xr;
+        const double top = (double)col[0], bot = (double)col[(size_t)(ny - 1) * p.px];
+        const double gt = bc == ABFT_BC_CLAMP ? top : (bc == ABFT_BC_PERIODIC ? bot : g);
+        const double gb = bc == ABFT_BC_CLAMP ? bot : (bc == ABFT_BC_PERIODIC ? top : g);
+        s = __dadd_rn(s, dj < 0 ? __dsub_rn(gt, bot) : __dsub_rn(gb, top));
+      }
+      Sv[q] = s;
+    } else {
+      const int ys = e + dj;
+      const bool yg = ghostv && (ys < 0 || ys >= ny);
+      if (L.zg[d] || yg) {
+        Sv[q] = __dmul_rn((double)nx, g);
+        continue;
+      }
+      const int yr = (ys >= 0 && ys < ny) ? ys : (bc == ABFT_BC_PERIODIC ? wrap(ys, ny) : max(0, min(ys, ny - 1)));
+      double s = L.prow[d][yr];
+      if (di != 0) {   // beta: the x-edge columns of u^{s-1} (ledger, or the halo layer itself)
+        double lft, rgt;
+        if (L.exl[d]) {
+          lft = (double)L.exl[d][yr];
+          rgt = (double)L.exr[d][yr];
+        } else {
+          const T* row = L.lay[d] + (size_t)yr * p.px;
+          lft = (double)row[0];
+          rgt = (double)row[nx - 1];
+        }
+        const double gl = bc == ABFT_BC_CLAMP ? lft : (bc == ABFT_BC_PERIODIC ? rgt : g);
+        const double gr = bc == ABFT_BC_CLAMP ? rgt : (bc == ABFT_BC_PERIODIC ? lft : g);
+        s = __dadd_rn(s, di < 0 ? __dsub_rn(gl, rgt) : __dsub_rn(gr, lft));
+      }
+      Sv[q] = s;
+    }
+  }
+  double acc = L.crow[e];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) acc = __dadd_rn(acc, __dmul_rn(p.w[q], Sv[q]));
+  return acc;
+}
+
 // Eq. 1 for the one cell (z, y, x) of u^s from u^{s-1} (p.uprev), with the
 // ghosts of the boundary condition: the same canonical FMA chain as K1
 // (points in order, then the sources).  correction_form 2.
@@ -524,13 +622,17 @@ __device__ __forceinline__ void check_vec(const CheckParams& p, int z, int* s_n,
   double* fwd1 = z == p.zc - 1 ? (A ? p.fwdA[1] : p.fwdB[1]) : nullptr;
   const bool fwd_pred = p.flags & CK_STORE_PRED;
   constexpr int KU = check_unroll<S>();
+  constexpr bool GEN = S == SHAPE_GENERIC;
+  const PredLayer<T, A> PL = pred_layer<T, A, BCG>(p, z);   // (unused by the generic list)
+  (void)PL;
   for (int e0 = lo + threadIdx.x; e0 < n; e0 += kCheckThreads * KU) {
     double pr[KU], ac[KU];
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
       const int e = e0 + u * kCheckThreads;
       const bool in = e < n;
-      pr[u] = in ? predict_entry<T, S, A, BCG>(p, z, e) : 0.0;
+      if constexpr (GEN) pr[u] = in ? predict_entry<T, S, A, BCG>(p, z, e) : 0.0;
+      else pr[u] = in ? predict_entry_l<T, (GEN ? SHAPE_HOTSPOT7 : S), A, BCG>(p, PL, e) : 0.0;
       ac[u] = (in && cmp) ? act[(size_t)bz * nn + e] : 0.0;
     }
 #pragma unroll
