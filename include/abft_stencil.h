@@ -78,8 +78,10 @@ typedef enum { ABFT_MODE_NONE = 0, ABFT_MODE_ONLINE = 1, ABFT_MODE_OFFLINE = 2 }
  * checksums.  If one or more errors are detected, only then ... interpolate
  * the other checksum"): b every sweep; for a layer whose b flags, a^{s-1} and
  * a^s are computed from the fields and a' compared, to locate and correct.
- * OFFLINE windows and the explicit sweep()/check()/correct() API always use
- * BOTH. */
+ * OFFLINE windows under LAZY predict, sum and compare b alone: a window is
+ * rolled back, never corrected, so a is never needed (Q29; dirty
+ * records carry nflag_a = 0, x = -1).  The explicit sweep()/check()/correct()
+ * API always uses BOTH. */
 typedef enum { ABFT_CK_BOTH = 0, ABFT_CK_LAZY = 1 } abft_checksum_policy;
 /* What a dirty OFFLINE window re-executes.  ROLLBACK: the whole window from
  * its checkpoint.  PARTIAL: stencil locality (P:107-108,
@@ -160,7 +162,7 @@ typedef struct {
                               cells rewritten and a, b of the layer re-summed
                               (Q27) */
   int32_t rank, nranks; /* z-slab decomposition; nranks == 1: single process */
-  int32_t checksum_policy; /* abft_checksum_policy (ONLINE step() only) */
+  int32_t checksum_policy; /* abft_checksum_policy (ONLINE and OFFLINE step()) */
   const void* nccl_unique_id; /* host pointer to a 128-byte ncclUniqueId shared by
                                  all ranks (one process per GPU, nranks > 1); NULL
                                  for nranks == 1 or for a local group member (see
@@ -346,7 +348,8 @@ int abft_stencil_set_faults(abft_stencil* h, const abft_fault* faults, int32_t n
 int abft_stencil_field(abft_stencil* h, void** dev_ptr, int64_t* pitch);
 /* copy the current slab, dense [z_count][ny][nx], to dst (HOST or DEVICE) */
 int abft_stencil_read_field(abft_stencil* h, void* dst);
-/* copy the current actual checksums A [z_count][nx], B [z_count][ny] (HOST or DEVICE) */
+/* copy the current actual checksums A [z_count][nx], B [z_count][ny] (HOST or DEVICE);
+   under LAZY (a not carried) A is summed from the current field first */
 int abft_stencil_checksums(abft_stencil* h, double* A, double* B);
 int abft_stencil_stats(abft_stencil* h, abft_stats* out);
 /* copy up to cap records (in device append order) to the host array out;
