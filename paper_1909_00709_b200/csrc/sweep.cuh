@@ -382,11 +382,23 @@ __device__ __forceinline__ void load_row(T (&W)[16 / sizeof(T) + 2], const unsig
   ld_vec<T, V>(c, reinterpret_cast<const T*>(slot + sro));
 #pragma unroll
   for (int k = 0; k < V; ++k) W[k + 1] = c[k];
+  if constexpr (sizeof(T) == 8) {
+    // fp64: the x neighbours straight from the staged row (lane 0 / 31 read
+    // the tile's halo) -- two shared loads instead of two 64-bit shuffles,
+    // a broadcast load and two 64-bit selects (cfg5 K1: instructions -13%,
+    // 1.488 -> 1.404 ms, shared wavefronts +18%; round 1 measured the
+    // opposite when every staged row was loaded three times)
+    W[0] = *reinterpret_cast<const T*>(slot + sro - (int)sizeof(T));
+    W[V + 1] = *reinterpret_cast<const T*>(slot + sro + V * (int)sizeof(T));
+    (void)seo;
+    (void)lane;
+  } else {
   const T e = *reinterpret_cast<const T*>(slot + seo);
   T left = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
   T right = __shfl_down_sync(0xffffffffu, c[0], 1);
   W[0] = lane == 0 ? e : left;
   W[V + 1] = lane == 31 ? e : right;
+  }
   if constexpr (EDGE) {
     if (ec.bc == ABFT_BC_CLAMP) {
       if (gx0 == 0) W[0] = W[1];
