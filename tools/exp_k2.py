@@ -1,12 +1,12 @@
 """Experiment variants of the K2 translation unit (not the product): rebuild
 only k2_check.cu with -D switches and link it with the product's other
 objects.   python tools/exp_k2.py NAME -DABFT_KU_FEW=4 ...
-writes paper_1909_00709_b200/exp/libabft_NAME.so"""
+writes tools/explib/libabft_NAME.so (it travels to the GPU box)"""
 import glob, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1909_00709_b200 import build as B
 name, defs = sys.argv[1], sys.argv[2:]
-out = os.path.join(B.HERE, "exp")
+out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "explib")
 os.makedirs(out, exist_ok=True)
 B.build()
 src = os.path.join(B.CSRC, "k2_check.cu")
