@@ -19,10 +19,10 @@ B4="python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e"
 B5="python bench.py --config cfg5 --steps 5 --warmup 3 --no-cpu --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4.csv $B4 > /dev/null 2>&1; echo l4=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg5.csv $B5 > /dev/null 2>&1; echo l5=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_sweep -s 2 -c 1 -o /tmp/nc/k1_cfg4_lazy $B4 > gpurun_out/ncu_k1_4.log 2>&1; echo n4=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_check -s 2 -c 1 -o /tmp/nc/k2_cfg4_lazy $B4 > gpurun_out/ncu_k2_4.log 2>&1; echo n42=$?
-timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:_ZN4abft8k1_sweepIfLi4ELi0ELi0E -s 2 -c 1 -o /tmp/nc/k1_cfg4_none $B4 > gpurun_out/ncu_k1_4n.log 2>&1; echo n4n=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_sweep -s 30 -c 1 -o /tmp/nc/k1_cfg5 $B5 > gpurun_out/ncu_k1_5.log 2>&1; echo n5=$?
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:k1_sweep -s 2 -c 1 -o /tmp/nc/k1_cfg4_lazy $B4 > gpurun_out/ncu_k1_4.log 2>&1; echo n4=$?
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:k2_check -s 2 -c 1 -o /tmp/nc/k2_cfg4_lazy $B4 > gpurun_out/ncu_k2_4.log 2>&1; echo n42=$?
+timeout 600 ncu -f --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:_ZN4abft8k1_sweepIfLi4ELi0ELi0E -s 2 -c 1 -o /tmp/nc/k1_cfg4_none $B4 > gpurun_out/ncu_k1_4n.log 2>&1; echo n4n=$?
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:k1_sweep -s 30 -c 1 -o /tmp/nc/k1_cfg5 $B5 > gpurun_out/ncu_k1_5.log 2>&1; echo n5=$?
 for r in k1_cfg4_lazy k1_cfg4_none k2_cfg4_lazy k1_cfg5; do python tools/ncu_summary.py /tmp/nc/$r.ncu-rep > gpurun_out/$r.txt 2>&1; python tools/ncu_summary.py --sass /tmp/nc/$r.ncu-rep >> gpurun_out/$r.txt 2>&1; cp /tmp/nc/$r.ncu-rep gpurun_out/; done
 python tools/ncu_summary.py --launches gpurun_out/launches_cfg4.csv > gpurun_out/launches_summary.txt
 python tools/ncu_summary.py --launches gpurun_out/launches_cfg5.csv >> gpurun_out/launches_summary.txt
