@@ -352,6 +352,13 @@ struct abft_stencil {
   int64_t launches = 0;
   int64_t rollbacks = 0, windows = 0, persistent = 0;
   int host_worst = 0;
+  // offline, single slab: while the host waits for window w's verdict the GPU
+  // already runs sweep 1 of window w + 1 (into the buffer that is neither
+  // w's checkpoint nor its result); kept if w is clean, dropped otherwise
+  bool spec_on = true;              // ABFT_OFFLINE_SPEC=0: wait idle instead
+  bool spec_done = false;           // sweep 1 of the next window has run
+  int* pin_dirty = nullptr;         // pinned host copy of the window verdict
+  cudaEvent_t ev_verdict = nullptr;
   std::vector<PendingFault> faults;
   ncclComm_t comm = nullptr;
   // multi-process job over CUDA IPC (abft_stencil_ipc_link): neighbour proxies
@@ -1038,14 +1045,65 @@ int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, 
 // its checkpoint (rotation of three field buffers: no copy), or only the
 // light cone of the flagged layers (recovery PARTIAL); a second mismatch is a
 // persistent error.
-int offline_window(Group& G, int L) {
+// sweep 1 of the window after this one, run while the host waits for this
+// window's verdict (single slab): from this window's result `last` into the
+// buffer that is neither `last` nor this window's checkpoint `ck`, predicting
+// from this window's actual checksums into slot 1 -- exactly what the next
+// window's first sweep does, so the next window adopts it (the buffer order
+// below makes that sweep write the same buffer).  No flip may be scheduled in
+// it (a dropped speculation would have consumed it).
+bool spec_allowed(const abft_stencil* h, int64_t s) {
+  if (!h->spec_on || h->cfg.nranks != 1 || h->grouped || h->ipc || h->prof) return false;
+  for (const PendingFault& pf : h->faults)
+    if (!pf.fired && pf.f.sweep == s) return false;
+  return true;
+}
+int spec_sweep(abft_stencil* h, int ck, int last, int gend, int64_t s) {
+  const int x = 3 - ck - last;
+  const int bf = h->cfg.checksum_policy == ABFT_CK_LAZY ? CK_BONLY : 0;
+  TRY(launch_k1(h, last, x, nullptr, nullptr, K1_CK_NONE, s));
+  TRY(launch_check(h, last, x, h->gA[gend], h->gB[gend], nullptr, nullptr, h->PA[1], h->PB[1], nullptr,
+                   nullptr, CK_STORE_PRED | bf, s));
+  return ABFT_OK;
+}
+// the window verdict of a single slab: copied to pinned memory behind the
+// window's check, then (after the caller enqueued more work) waited for
+int verdict_post(abft_stencil* h) {
+  on_dev(h);
+  if (!h->pin_dirty) CK(cudaHostAlloc(reinterpret_cast<void**>(&h->pin_dirty), 4 * sizeof(int), cudaHostAllocDefault));
+  if (!h->ev_verdict) CK(cudaEventCreateWithFlags(&h->ev_verdict, cudaEventDisableTiming));
+  CK(cudaMemcpyAsync(h->pin_dirty, &h->st->dirty, 3 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaEventRecord(h->ev_verdict, h->stream));
+  return ABFT_OK;
+}
+int verdict_wait(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
+  CK(cudaEventSynchronize(h->ev_verdict));
+  *dirty = h->pin_dirty[0];
+  *zmin = 0x7fffffffLL - h->pin_dirty[1];
+  *zmax = (int64_t)h->pin_dirty[2] - 1;
+  return ABFT_OK;
+}
+
+int offline_window(Group& G, int L, bool spec_next) {
   abft_stencil* h0 = G[0];
   const int ck = h0->cur, ckgen = h0->gen, gend = (h0->gen + 1) % kGens;
   const int64_t s0 = h0->sweeps;
   const bool partial = h0->cfg.recovery == ABFT_RECOVER_PARTIAL;
+  // the two buffers besides the checkpoint, the one that is not the previous
+  // window's checkpoint first (a speculative first sweep wrote it, see above)
   int others[2], k = 0;
   for (int b = 0; b < 3; ++b)
-    if (b != ck) others[k++] = b;
+    if (b != ck && b != h0->prev) others[k++] = b;
+  for (int b = 0; b < 3; ++b)
+    if (b != ck && b == h0->prev) others[k++] = b;
+  if (k != 2) {   // prev == ck (first window after init): plain order
+    k = 0;
+    for (int b = 0; b < 3; ++b)
+      if (b != ck) others[k++] = b;
+  }
+  const bool adopt = h0->spec_done;   // sweep 1 already ran (previous window's speculation)
+  h0->spec_done = false;
+  const bool single = G.size() == 1 && h0->cfg.nranks == 1;
   int last = ck;
   int worst = ABFT_OK;
   int64_t zlo = 0, zhi = 0;
@@ -1068,9 +1126,11 @@ int offline_window(Group& G, int L) {
           const bool bonly = h->cfg.checksum_policy == ABFT_CK_LAZY;
           const int bf = bonly ? CK_BONLY : 0;
           if (!end) {
-            TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
-            TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
-                             nullptr, nullptr, CK_STORE_PRED | bf, s));
+            if (!(adopt && attempt == 0 && t == 1)) {
+              TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s));
+              TRY(launch_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[t & 1], h->PB[t & 1],
+                               nullptr, nullptr, CK_STORE_PRED | bf, s));
+            }
           } else {
             TRY(zero_gen(h, gend));
             TRY(launch_k1(h, src, dst, bonly ? nullptr : h->gA[gend], h->gB[gend], bonly ? K1_CK_B : K1_CK_AB,
@@ -1088,9 +1148,20 @@ int offline_window(Group& G, int L) {
     }
     int dirty = 0;
     int64_t zmin = 0, zmax = 0;
-    TRY(read_dirty(G, &dirty, &zmin, &zmax));
+    const bool spec = single && spec_next && attempt == 0 && spec_allowed(h0, s0 + L + 1);
+    if (single) {
+      TRY(verdict_post(h0));
+      if (spec) TRY(spec_sweep(h0, ck, last, gend, s0 + L + 1));
+      TRY(verdict_wait(h0, &dirty, &zmin, &zmax));
+    } else {
+      TRY(read_dirty(G, &dirty, &zmin, &zmax));
+    }
     for (abft_stencil* h : G) h->windows++;
-    if (!dirty) break;
+    if (!dirty) {
+      h0->spec_done = spec;
+      break;
+    }
+    if (spec) h0->executed--;   // the speculative sweep is dropped (it ran on a dirty result)
     if (attempt == 0) {
       // re-execution range of a partial recovery: every layer an error of
       // this window that was flagged can have reached (Q28)
@@ -1281,7 +1352,9 @@ int step_group(Group& G, int32_t n) {
     int worst = ABFT_OK;
     while (n > 0) {
       const int L = std::min<int>(n, G[0]->cfg.delta);
-      int r = offline_window(G, L);
+      // the next window's first sweep may run while this window's verdict
+      // is read back when that window has an in-window sweep (length >= 2)
+      int r = offline_window(G, L, n - L >= 2 && G[0]->cfg.delta >= 2);
       if (r < 0) return r;
       worst = std::max(worst, r);
       n -= L;
@@ -1608,6 +1681,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->launches += 4;
   h->zmask = ((1u << kGens) - 1) & ~1u;   // aux cleared, K0 wrote generation 0
   if (const char* e = getenv("ABFT_GRAPHS")) h->graphs_on = atoi(e) != 0;
+  if (const char* e = getenv("ABFT_OFFLINE_SPEC")) h->spec_on = atoi(e) != 0;
   if (const char* e = getenv("ABFT_PIPE_PDL")) h->pipe_pdl = atoi(e) != 0;
   if (h->pipe) {
     int lo = 0, hi = 0;
@@ -2066,6 +2140,8 @@ int abft_stencil_destroy(abft_stencil* h) {
   if (h->s2) { cudaStreamSynchronize(h->s2); cudaStreamDestroy(h->s2); }
   for (StepGraph& g : h->graphs) { cudaGraphExecDestroy(g.exec); cudaGraphDestroy(g.graph); }
   if (h->cs) cudaStreamDestroy(h->cs);
+  if (h->ev_verdict) cudaEventDestroy(h->ev_verdict);
+  if (h->pin_dirty) cudaFreeHost(h->pin_dirty);
   for (cudaEvent_t e : {h->ev_k1, h->ev_chk[0], h->ev_chk[1]})
     if (e) cudaEventDestroy(e);
   if (h->ev_ready) cudaEventDestroy(h->ev_ready);
