@@ -253,8 +253,8 @@ def run_ours(a):
     idx = vis.split(",")[local] if vis and vis.split(",")[local].isdigit() else str(local)
     clocks = Clocks(idx)
 
-    def protected_run(mode, with_faults, prof=False, policy=pol):
-        st = new_handle(p, u0, P, device=dev, stream=stream, mode=mode, checksum_policy=policy)
+    def protected_run(mode, with_faults, prof=False, policy=pol, prob=None):
+        st = new_handle(prob or p, u0, P, device=dev, stream=stream, mode=mode, checksum_policy=policy)
         if with_faults:
             st.set_faults(shift(faults, W))
         st.step(W)
@@ -287,6 +287,10 @@ def run_ours(a):
     with torch.cuda.stream(stream):
         rA = protected_run(pmode, True)               # headline: flips on
         rE = protected_run(pmode, True, policy=pol_other)
+        # offline: the same flipped run re-executing only the flagged layers'
+        # light cone on a dirty window (recovery PARTIAL, DESIGN Q28)
+        # instead of the whole window (bitwise the same result)
+        rP = protected_run(pmode, True, prob=p.replace(recovery=1)) if pmode == 2 else None
         # overhead (t_protected / t_unprotected - 1, error-free runs): the
         # three error-free runs interleaved, 7 rounds, median of each (clocks
         # drift under the power cap; interleaving exposes every run to it alike)
@@ -307,6 +311,7 @@ def run_ours(a):
     tC = max_over_ranks(rC["ms"], world)
     tD = max_over_ranks(rD["ms"], world)
     tE = max_over_ranks(rE["ms"], world)
+    tP = max_over_ranks(rP["ms"], world) if rP is not None else None
     value = cells_global * K / (tA * 1e-3) / 1e9
     # roofline of the dominant kernel K1 (protected, checksums fused): algorithmic
     # bytes = (field read + source read + field write) * cells of the launch
@@ -414,6 +419,12 @@ def run_ours(a):
                              "protected_gcells_with_flips": round(cells_global * K / (tE * 1e-3) / 1e9, 3),
                              "k1_ms": round(k1_ms_other, 5), "check_ms_per_sweep": round(k2_ms_other, 5),
                              "detections": rE["stats"]},
+            "offline_partial_recovery": None if tP is None else {
+                "what": "the headline's flipped run with recovery PARTIAL: a dirty window re-executes "
+                        "only the flagged layers' light cone (P:743-745, DESIGN.md Q28)",
+                "protected_gcells_with_flips": round(cells_global * K / (tP * 1e-3) / 1e9, 3),
+                "abft_overhead_with_flips_pct": round((tP / tC - 1.0) * 100.0, 3),
+                "detections": rP["stats"]},
             "unprotected_gcells": round(cells_global * K / (tC * 1e-3) / 1e9, 3),
             "error_free_protected_gcells": round(cells_global * K / (tB * 1e-3) / 1e9, 3),
             "hbm_roofline_frac_step": round(value * 1e9 * bytes_cell / (peak * 1e9) / world, 4),

@@ -709,3 +709,227 @@ def test_offline_b_only_equals_both_when_b_flags():
     assert [strip(q) for q in bonly["records"]] == [strip(q) for q in both["records"]]
     assert all(q["nflag_a"] == 0 and q["x"] == -1 for q in bonly["records"])
     assert all(q["nflag_b"] >= 1 for q in bonly["records"])
+
+
+# ------------------------- exact-arithmetic pins of the fp32 rounding (Q23)
+
+def _r32(q: Fraction) -> float:
+    """q rounded once to the nearest fp32 (ties to even) -- IEEE 754's
+    definition of a correctly rounded operation, in exact rational arithmetic
+    (independent of the hardware and of the oracle)."""
+    if q == 0:
+        return 0.0
+    s, a = (-1 if q < 0 else 1), abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    ulp = Fraction(2) ** (max(e, -126) - 23)
+    m = a / ulp
+    n = m.numerator // m.denominator
+    rem = m - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    return float(s * n * ulp)
+
+
+def _f(v) -> Fraction:
+    return Fraction(float(np.float32(v)))
+
+
+def test_r32_rounding_helper_matches_numpy():
+    # the helper above against numpy's fp64 -> fp32 cast (exact inputs)
+    rng = np.random.default_rng(3)
+    for v in list(rng.normal(size=200) * 1e3) + [1 + 2 ** -24, 1 + 3 * 2 ** -24, 2 ** -140 * 1.3]:
+        assert _r32(Fraction(float(v))) == float(np.float32(v))
+
+
+@pytest.mark.parametrize("srcs,base,span", [
+    ([(0.001, True, 0.0), (0.05, False, 80.0)], 323.0, 20.0),    # HotSpot (cfg2-4)
+    ([(0.7, True, 0.0), (0.3, False, 1.7)], 0.0, 1.0),           # sources of the size of the field
+])
+def test_fp32_sweep_is_the_fused_canonical_chain(srcs, base, span):
+    # Q23 (SURVEY §8(c) C2): an fp32 cell is acc = w_0 v_0, acc = fma(w_p, v_p,
+    # acc) over the points in order, then acc = fma(coef_q, src_q, acc): each
+    # step ONE rounding of the exact w*v + acc.  Evaluated here in exact
+    # rationals with _r32, cell by cell (HotSpot weights, non-dyadic, clamp);
+    # the unfused chain (w*v rounded, then the add rounded) differs in many
+    # cells, so the pin can fail.
+    pts = [(0, 0, 0, 0.4), (-1, 0, 0, 0.1), (1, 0, 0, 0.1), (0, -1, 0, 0.1), (0, 1, 0, 0.1),
+           (0, 0, -1, 0.05), (0, 0, 1, 0.05)]
+    nz, ny, nx = 3, 5, 6
+    p = Problem("t", nx, ny, nz, "f32", pts, srcs)
+    rng = np.random.default_rng(11)
+    u = (base + span * rng.random((nz, ny, nx))).astype(np.float32)
+    P = rng.random((nz, ny, nx)).astype(np.float32)
+    out = O.sweep(O.OProblem(p, [P]), u)
+    cl = lambda c, n: min(max(c, 0), n - 1)
+    unfused_differs = [0, 0]   # chain, sources
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                acc = accu = None
+                for di, dj, dk, w in pts:
+                    v = Fraction(float(u[cl(z + dk, nz), cl(y + dj, ny), cl(x + di, nx)]))
+                    t = _f(w) * v
+                    acc = _r32(t) if acc is None else _r32(t + Fraction(acc))
+                    accu = _r32(t) if accu is None else _r32(Fraction(_r32(t)) + Fraction(accu))
+                unfused_differs[0] += accu != acc
+                accs = acc
+                for (cf, fld, sc) in srcs:
+                    sv = Fraction(float(P[z, y, x])) if fld else _f(sc)
+                    acc = _r32(_f(cf) * sv + Fraction(acc))
+                    accs = _r32(Fraction(_r32(_f(cf) * sv)) + Fraction(accs))
+                assert float(out[z, y, x]) == acc, (z, y, x)
+                unfused_differs[1] += accs != acc
+    assert unfused_differs[0] > 0 and (base > 0 or unfused_differs[1] > 0)
+
+
+def test_constant_sums_fp32_round_the_scalar_too():
+    # c_x, c_y (P:321, P:392) of an fp32 problem whose scalar source is not an
+    # fp32 value (80.3): C is built from the dtype-rounded scalar, as the sweep
+    # applies it (Q23); exact rational brute force as in the pin above.
+    nz, ny, nx = 2, 5, 7
+    p = Problem("t", nx, ny, nz, "f32", [(0, 0, 0, 1.0)], [(0.001, True, 0.0), (0.05, False, 80.3)])
+    P = np.random.default_rng(6).random((nz, ny, nx)).astype(np.float32)
+    cA, cB = O.constant_sums(O.OProblem(p, [P]))
+    C = [[[_f(0.001) * Fraction(float(P[z, y, x])) + _f(0.05) * _f(80.3) for x in range(nx)]
+          for y in range(ny)] for z in range(nz)]
+    for z in range(nz):
+        for x in range(nx):
+            ex = sum(C[z][y][x] for y in range(ny))
+            assert abs(Fraction(cA[z, x]) - ex) <= ex * Fraction(1, 2 ** 49)
+        for y in range(ny):
+            ex = sum(C[z][y][x] for x in range(nx))
+            assert abs(Fraction(cB[z, y]) - ex) <= ex * Fraction(1, 2 ** 49)
+    raw = sum(_f(0.001) * Fraction(float(P[0, y, 0])) + _f(0.05) * Fraction(80.3) for y in range(ny))
+    assert abs(Fraction(cA[0, 0]) - raw) > raw * Fraction(1, 10 ** 10)
+
+
+@pytest.mark.parametrize("bc", [0, 1, 3])
+def test_theorem1_fp32_exact_linear_update(bc):
+    # Theorem 1 (P:314-336) is an identity of the linear update: a'_x equals
+    # the column sum of sum_q w_q u(neighbour) + C EXACTLY, for the weights the
+    # sweep uses -- fp32-rounded for an fp32 problem (Q23).  The right side is
+    # brute force in exact rationals (the stencil applied cell by cell, every
+    # ghost read through the BC, then summed); the oracle's fp64 prediction may
+    # differ from it only by its own rounding (~1e-15), while unrounded fp64
+    # weights (0.1 vs fp32 0.1) would be off by ~1e-9.
+    pts = [(0, 0, 0, 0.35), (-1, 0, 0, 0.1), (1, 0, 0, 0.15), (0, -1, 0, 0.1), (0, 1, 0, 0.05),
+           (1, 1, 0, 0.1), (0, 0, -1, 0.05), (-1, 0, 1, 0.1)]
+    srcs = [(0.001, True, 0.0), (0.05, False, 80.0)]
+    nz, ny, nx = 3, 5, 6
+    g = 330.5
+    p = Problem("t", nx, ny, nz, "f32", pts, srcs, bc=bc, bc_value=g)
+    rng = np.random.default_rng(12 + bc)
+    u = (323 + 20 * rng.random((nz, ny, nx))).astype(np.float32)
+    P = rng.random((nz, ny, nx)).astype(np.float32)
+    op = O.OProblem(p, [P])
+    A, B = O.checksums(op, u)
+    PA, PB = O.predict(op, A, B, u)
+
+    def val(z, y, x):
+        if bc == 1:
+            return Fraction(float(u[z % nz, y % ny, x % nx]))
+        if bc == 0:
+            return Fraction(float(u[min(max(z, 0), nz - 1), min(max(y, 0), ny - 1), min(max(x, 0), nx - 1)]))
+        if 0 <= z < nz and 0 <= y < ny and 0 <= x < nx:
+            return Fraction(float(u[z, y, x]))
+        return _f(g)
+    lin = [[[sum(_f(w) * val(z + dk, y + dj, x + di) for di, dj, dk, w in pts)
+             + _f(0.001) * Fraction(float(P[z, y, x])) + _f(0.05) * _f(80.0)
+             for x in range(nx)] for y in range(ny)] for z in range(nz)]
+    for z in range(nz):
+        for x in range(nx):
+            ex = sum(lin[z][y][x] for y in range(ny))
+            assert abs(Fraction(PA[z, x]) - ex) <= ex * Fraction(1, 10 ** 13), (z, x)
+        for y in range(ny):
+            ex = sum(lin[z][y][x] for x in range(nx))
+            assert abs(Fraction(PB[z, y]) - ex) <= ex * Fraction(1, 10 ** 13), (z, y)
+
+
+# ----------------------- forms 0 / 1 with several flags (Q13, Q14, P:663-667)
+
+def test_several_flags_in_a_layer_record_first_row_and_column_uncorrectable():
+    # P:663-667: several errors in one layer pair up ambiguously -- forms 0 / 1
+    # do not correct them (Q13: |X| >= 2 or |Y| >= 2 is "uncorrectable"), and
+    # the record names the first flagged row and column (P:232-234, lowest
+    # index) with the flag counts; the field keeps both flipped values.
+    p = make_problem("cfg2", nx=40, ny=36, nz=4, sweeps=6)
+    op = O.OProblem(p, [field_power(p).numpy()])
+    u0 = field_u0(p).numpy()
+    ref = O.run(op, u0, 4)
+    for form in (0, 1):
+        q = p.replace(correction_form=form)
+        r = O.run(O.OProblem(q, [field_power(q).numpy()]), u0, 4,
+                  [Fault(4, 2, 20, 31, 29), Fault(4, 2, 7, 9, 29)])
+        assert r["status"] == 1 and r["stats"]["uncorrectable"] == 1 and r["stats"]["corrected"] == 0
+        (rec,) = r["records"]
+        assert rec["status"] == O.REC_UNCORRECTABLE
+        assert (rec["sweep"], rec["z"], rec["y"], rec["x"]) == (4, 2, 7, 9)
+        assert (rec["nflag_a"], rec["nflag_b"]) == (2, 2)
+        diff = np.argwhere(r["u"].view(np.uint32) != ref["u"].view(np.uint32))
+        assert sorted(map(tuple, diff)) == [(2, 7, 9), (2, 20, 31)]
+
+
+def test_flag_in_one_vector_only_is_unlocated():
+    # fig.abft.error scenario 2 (P:638, Q14): a flip that moves its column sum
+    # (ny = 8 terms) past eps but not its row sum (nx = 256 terms) flags a
+    # alone: detected, not located.  delta = 2^(12 - 15) = 0.125 on a value in
+    # [256, 512): column |d| / S ~ 0.125 / 2640 > 1e-5 > row 0.125 / 84480.
+    p = make_problem("cfg2", nx=256, ny=8, nz=2, sweeps=3)
+    op = O.OProblem(p, [field_power(p).numpy()])
+    r = O.run(op, field_u0(p).numpy(), 3, [Fault(2, 1, 5, 100, 12)])
+    (rec,) = r["records"]
+    assert rec["status"] == O.REC_UNLOCATED and r["stats"]["unlocated"] == 1 and r["status"] == 1
+    assert (rec["nflag_a"], rec["nflag_b"]) == (1, 0) and rec["x"] == 100
+
+
+def test_literal_form_corrects_and_repairs_a_mantissa_flip():
+    # fig.correction as listed (P:670-677, form 1) on a mantissa flip: the
+    # corrected value is the clean one within the checksum's rounding, and the
+    # repaired a, b (a += c - u, P:654) are the true sums of the repaired
+    # layer, so no later sweep flags (one detection in the whole run).
+    p = make_problem("cfg2", nx=48, ny=40, nz=3, sweeps=6).replace(correction_form=1)
+    op = O.OProblem(p, [field_power(p).numpy()])
+    u0 = field_u0(p).numpy()
+    clean = _clean_states(p, op, u0, 3)[1, 17, 23]
+    r = O.run(op, u0, 6, [Fault(3, 1, 17, 23, 20)])
+    assert r["stats"]["detections"] == 1 and r["stats"]["corrected"] == 1
+    (rec,) = r["records"]
+    assert (rec["y"], rec["x"]) == (17, 23)
+    assert abs(rec["corrected"] - clean) / clean < 1e-6
+    A1, B1 = _fsum_checksums(r["u"])
+    assert np.max(np.abs(r["A"] - A1) / A1) < 1e-9 and np.max(np.abs(r["B"] - B1) / B1) < 1e-9
+
+
+# ------------------- partial re-execution: the 2 (L - 1) reach is needed (Q28)
+
+@pytest.mark.parametrize("bc,z0", [(0, 8), (1, 1)])
+def test_partial_reach_covers_errors_on_the_unflagged_side(bc, z0):
+    # An upwind stencil in z (u^s[z] = 0.98 u[z-1] + 1e-4 u[z+1]): a mantissa
+    # flip in layer z0 at a window's first sweep travels up, so after the
+    # window (L = 3 sweeps) only layer z0 + 2 flags, while the back-leak has
+    # put sub-threshold (fp64-visible) errors in layers z0 and z0 - 2.  Those
+    # lie 4 = 2 (L - 1) layers below the flagged one: the re-executed range
+    # must reach them for the partial re-execution to equal the full rollback
+    # bitwise (P:743-745 via Q28); a reach of L - 1 would leave z0 - 2
+    # contaminated.  Periodic z (bc 1, z0 = 1): the reach wraps to the top
+    # layer, so every layer is re-executed.
+    pts = [(0, 0, -1, 0.98), (0, 0, 1, 1e-4)]
+    p = Problem("t", 8, 8, 16, "f64", pts, [], bc=bc, eps=1e-4, mode=2, delta=3, sweeps=3,
+                init=(1.0, 2.0))
+    op = O.OProblem(p)
+    u0 = field_u0(p).numpy()
+    f = [Fault(1, z0, 3, 4, 50)]
+    clean = O.run(O.OProblem(p.replace(mode=0)), u0, 1)["u"]
+    first = O.run(O.OProblem(p.replace(mode=0)), u0, 3, f)["u"]
+    ref = O.run(O.OProblem(p.replace(mode=0)), u0, 3)["u"]
+    bad = sorted({int(z) for z, _, _ in np.argwhere(first != ref)})
+    assert bad == sorted({(z0 - 2) % 16, z0, z0 + 2}), bad
+    assert clean[z0, 3, 4] != 0
+    full = O.run(op, u0, 3, f)
+    part = O.run(O.OProblem(p.replace(recovery=1)), u0, 3, f)
+    assert [(r["z"], r["status"]) for r in full["records"]] == [(z0 + 2, O.REC_WINDOW_DIRTY)]
+    for r in (full, part):
+        assert r["stats"]["rollbacks"] == 1 and r["status"] == 0
+        assert (r["u"].view(np.uint64) == ref.view(np.uint64)).all()
