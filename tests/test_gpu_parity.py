@@ -577,3 +577,31 @@ def test_offline_partial_slab_group(G, halo):
     for s in g["stats"]:
         for k in ("sweeps", "rollbacks", "windows", "persistent"):
             assert s[k] == o["stats"][k], (k, s, o["stats"])
+
+
+@pytest.mark.parametrize("bc,z0", [(0, 8), (1, 1)])
+def test_offline_partial_reach_on_the_unflagged_side(bc, z0):
+    # the oracle pin test_partial_reach_covers_errors_on_the_unflagged_side at
+    # GPU scale (several x / y tiles): an upwind z stencil moves a flip's
+    # error up, so only layer z0 + 2 flags while sub-threshold errors sit in
+    # z0 and z0 - 2 (periodic: wrapped to the top) -- the re-executed range
+    # must reach them (Q28); the result equals the full rollback's
+    pts = [(0, 0, -1, 0.98), (0, 0, 1, 1e-4)]
+    p = Problem("t", 70, 40, 16, "f64", pts, [], bc=bc, eps=1e-4, mode=2, delta=3, sweeps=6,
+                init=(1.0, 2.0), recovery=1)
+    faults = [Fault(1, z0, 3, 4, 50), Fault(4, 12, 30, 60, 50)]
+    g, o = parity(p, faults=faults)
+    assert o["stats"]["rollbacks"] == 2
+    full = gpu_run(p.replace(recovery=0), faults=faults)
+    assert np.array_equal(g["u"].view(np.uint64), full["u"].view(np.uint64))
+
+
+def test_flag_in_one_vector_only_is_unlocated():
+    # P:638 / Q14: the column sum flags, the row sum does not (see the oracle pin)
+    for checksums in (0, 1):
+        p = make_problem("cfg2", nx=256, ny=8, nz=2, sweeps=3, checksums=checksums)
+        g, o = parity(p, faults=[Fault(2, 1, 5, 100, 12)])
+        if checksums == 0:
+            assert [r["status"] for r in o["records"]] == [2]
+        else:   # b does not flag: the lazy policy never looks at a
+            assert o["records"] == []
