@@ -87,11 +87,13 @@ typedef enum { ABFT_CK_BOTH = 0, ABFT_CK_LAZY = 1 } abft_checksum_policy;
  * its checkpoint.  PARTIAL: stencil locality (P:107-108,
  * P:743-745 "exploit stencil locality to reduce the re-execution cost"): an
  * error injected in a window of L sweeps spreads at most L - 1 layers, so
- * only the layers within 2 (L - 1) of a flagged layer (over all ranks) are
- * re-executed from the checkpoint -- the light cone of that range, sweep by
- * sweep -- and re-checked; every other layer keeps its first execution
- * (Q28).  Equal to ROLLBACK whenever every error of the window is
- * detected; an undetected one outside the range is not erased. */
+ * only the layers within 2 (L - 1) of a flagged layer (the union of those
+ * neighbourhoods over the flagged layers of all ranks: several disjoint
+ * ranges when the flags are clustered) are re-executed from the checkpoint
+ * -- the light cones of those ranges, sweep by sweep -- and re-checked;
+ * every other layer keeps its first execution (Q28).  Equal to
+ * ROLLBACK whenever every error of the window is detected; an undetected
+ * one outside those layers is not erased. */
 typedef enum { ABFT_RECOVER_ROLLBACK = 0, ABFT_RECOVER_PARTIAL = 1 } abft_recovery;
 /* Schedule of an ONLINE step() on a single slab (nranks == 1).  AUTO: when
  * init is given a third field buffer, the checks of sweep s (steps (2)-(5))
@@ -306,19 +308,22 @@ int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps)
  * neighbours' halo slots from K1 / K2 / K3, and orders the next sweep after
  * the neighbours' through the events (a rank publishes its sweep count in
  * its slot; a neighbour enqueues the wait once the count is there).  Offline
- * window verdicts and the extent of the flagged layers (partial
- * re-execution) are reduced over all ranks through the slots.  Every rank
+ * window verdicts and the flagged layers (partial re-execution) are reduced
+ * over all ranks through the slots.  Every rank
  * calls step() with the same counts (lockstep).  Errors: ABFT_EINVAL for a
  * handle that is grouped, has a communicator, has stepped, or a blob that
  * does not describe the expected neighbour; ABFT_ECUDA if a handle or event
  * cannot be opened. */
 #define ABFT_IPC_BLOB_BYTES 1024
+#define ABFT_IPC_ZWORDS 256   /* recovery PARTIAL over IPC: z_count <= 32 * ABFT_IPC_ZWORDS per rank */
 typedef struct {
   int64_t seq;        /* halo exchanges this rank has published */
   int64_t wseq;       /* offline windows whose verdict this rank has published */
   int64_t wdone;      /* offline windows this rank has reduced */
   int32_t val[2][3];  /* verdict per window parity: flagged layers, extent words */
-  int32_t pad[2];
+  int32_t z_begin;    /* this rank's slab (set by ipc_link) */
+  int32_t z_count;
+  uint32_t zbits[2][ABFT_IPC_ZWORDS];  /* per window parity: flagged layers of the slab, bit z - z_begin */
 } abft_ipc_slot;
 int abft_stencil_ipc_export(abft_stencil* h, void* blob);
 int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_blob, void* shm);

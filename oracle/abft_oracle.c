@@ -472,6 +472,8 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
        at its start. */
     void* ckpt = malloc(fb);
     void* first = p->recovery == 1 ? malloc(fb) : NULL;
+    char* redo = malloc((size_t)nz);      /* layers the re-execution replaces */
+    char* flagged = malloc((size_t)nz);   /* layers the last window check flagged */
     int64_t s = sweep0;
     const int64_t end = sweep0 + nsweeps;
     while (s < end) {
@@ -479,7 +481,7 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
       memcpy(ckpt, cur, fb);                         /* in-memory checkpoint */
       /* layers the window check covers: all, and after a partial
          re-execution only the re-executed ones (Q28) */
-      int64_t zlo = 0, zhi = nz - 1;
+      memset(redo, 1, (size_t)nz);
       for (int32_t attempt = 0; attempt < 2; attempt++) {
         memcpy(PA, Ap, sizeof(double) * nz * nx);    /* interpolation starts from */
         memcpy(PB, Bp, sizeof(double) * nz * ny);    /* the checkpoint's checksums */
@@ -493,17 +495,19 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
           stats->sweeps++;
         }
         if (attempt == 1 && p->recovery == 1) {
-          /* partial re-execution (Q28): only layers zlo..zhi come from the
-             re-execution; every other layer keeps the first execution's
-             values (no detected error reached it) */
+          /* partial re-execution (Q28): only the layers marked in redo come
+             from the re-execution; every other layer keeps the first
+             execution's values (no detected error reached it) */
           const size_t lb = (size_t)nx * ny * esz(p->dtype);
           for (int64_t z = 0; z < nz; z++)
-            if (z < zlo || z > zhi) memcpy((char*)cur + z * lb, (const char*)first + z * lb, lb);
+            if (!redo[z]) memcpy((char*)cur + z * lb, (const char*)first + z * lb, lb);
         }
         or_checksums(p, cur, An, Bn);
         stats->windows++;
-        int64_t dirty = 0, zmin = nz, zmax = -1;
-        for (int64_t z = zlo; z <= zhi; z++) {
+        int64_t dirty = 0;
+        memset(flagged, 0, (size_t)nz);
+        for (int64_t z = 0; z < nz; z++) {
+          if (!redo[z]) continue;
           int64_t na = 0, nb = 0, x0 = -1, y0 = -1;
           /* checksums 1 (Q29): detection by b alone -- a is never compared */
           if (p->checksums != 1)
@@ -513,8 +517,7 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
             if (or_flag(PB[z * ny + y], Bn[z * ny + y], p->eps)) { if (y0 < 0) y0 = y; nb++; }
           if (na + nb == 0) continue;
           dirty++;
-          if (z < zmin) zmin = z;
-          if (z > zmax) zmax = z;
+          flagged[z] = 1;
           stats->detections++;
           or_record r;
           memset(&r, 0, sizeof r);
@@ -529,15 +532,22 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
           if (p->recovery == 1) {
             /* stencil locality, reading Q28: an error
                injected in this window of L sweeps has spread at most L - 1
-               layers from its origin, and every flagged layer lies within
-               that reach, so everything it touched is within 2 (L - 1)
-               layers of a flagged one */
+               layers from its origin, and every layer it made flag lies
+               within that reach, so everything it touched is within
+               2 (L - 1) layers of a flagged one: the layers to re-execute
+               are the union of those neighbourhoods over the flagged layers */
             const int64_t r = 2 * (wend - s - 1);
-            zlo = zmin - r < 0 ? 0 : zmin - r;
-            zhi = zmax + r > nz - 1 ? nz - 1 : zmax + r;
+            int wraps = 0;
+            memset(redo, 0, (size_t)nz);
+            for (int64_t f = 0; f < nz; f++) {
+              if (!flagged[f]) continue;
+              if (f - r < 0 || f + r > nz - 1) wraps = 1;
+              for (int64_t z = f - r; z <= f + r; z++)
+                if (z >= 0 && z < nz) redo[z] = 1;
+            }
             /* periodic z: a reach past a face wraps to the far layers -- take
                every layer then */
-            if (p->bc == OR_BC_PERIODIC && (zmin - r < 0 || zmax + r > nz - 1)) { zlo = 0; zhi = nz - 1; }
+            if (p->bc == OR_BC_PERIODIC && wraps) memset(redo, 1, (size_t)nz);
             memcpy(first, cur, fb);
           }
           if (cur != ckpt) memcpy(cur, ckpt, fb);
@@ -553,6 +563,8 @@ int32_t or_run(const or_problem* p, void* u, double* Aout, double* Bout,
     }
     free(ckpt);
     free(first);
+    free(redo);
+    free(flagged);
   }
   if (cur != u) memcpy(u, cur, fb);
   free(tmp);

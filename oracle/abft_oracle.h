@@ -71,8 +71,9 @@ typedef struct {
   int32_t recovery;    /* offline, dirty window: 0 = roll back to the window's
                           checkpoint and re-execute it;
                           1 = re-execute only the layers an error detected in
-                          the window can have reached (stencil locality,
-                          P:107-108; Q28) */
+                          the window can have reached: those within 2 (L - 1)
+                          of a flagged layer (stencil locality, P:107-108,
+                          P:743-745; Q28) */
 } or_problem;
 
 /* flip bit `bit` of cell idx */

@@ -38,6 +38,7 @@ EXPORTS = ("abft_stencil_workspace_size", "abft_stencil_init", "abft_stencil_ste
            "abft_stencil_halo_plan", "abft_stencil_ipc_export", "abft_stencil_ipc_link",
            "abft_stencil_plan", "abft_stencil_field_buffers")
 IPC_BLOB_BYTES = 1024
+IPC_ZWORDS = 256
 
 
 class abft_point(C.Structure):
@@ -81,7 +82,8 @@ class abft_stats(C.Structure):
 
 class abft_ipc_slot(C.Structure):
     _fields_ = [("seq", C.c_int64), ("wseq", C.c_int64), ("wdone", C.c_int64),
-                ("val", (C.c_int32 * 3) * 2), ("pad", C.c_int32 * 2)]
+                ("val", (C.c_int32 * 3) * 2), ("z_begin", C.c_int32), ("z_count", C.c_int32),
+                ("zbits", (C.c_uint32 * IPC_ZWORDS) * 2)]
 
 
 class AbftError(RuntimeError):

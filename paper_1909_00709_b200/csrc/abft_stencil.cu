@@ -146,7 +146,7 @@ struct Layout {
   int64_t px, plane;
   size_t field_bytes;
   // aux offsets
-  size_t off_gA[kGens], off_gB[kGens], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_lazy, off_st, off_src;
+  size_t off_gA[kGens], off_gB[kGens], off_PA[2], off_PB[2], off_cA, off_cB, off_summ, off_lazy, off_st, off_src, off_zflag;
   size_t off_EX[3];  // x-edge ledger of each field buffer, [2][zc+2][ny] of dtype
   size_t aux_bytes;
   size_t hot_bytes;  // prefix of aux touched every sweep
@@ -274,6 +274,8 @@ Layout layout(const abft_config* c) {
   L.pad_src = fs >= 0 && ((c->nx * L.esz) % 16 != 0 ||
                           (reinterpret_cast<uintptr_t>(c->sources[fs].field) % 16) != 0);
   L.off_src = L.pad_src ? take((size_t)L.plane * c->z_count * L.esz) : 0;
+  // offline: one word per global layer, set by a window check that flags it
+  L.off_zflag = take((size_t)c->nz_global * sizeof(int));
   L.aux_bytes = o;
   return L;
 }
@@ -352,6 +354,7 @@ struct abft_stencil {
   int64_t launches = 0;
   int64_t rollbacks = 0, windows = 0, persistent = 0;
   int host_worst = 0;
+  int* zflag = nullptr;    // [nz_global] offline: layers the last window check flagged (Q28)
   // offline, single slab: while the host waits for window w's verdict the GPU
   // already runs sweep 1 of window w + 1 (into the buffer that is neither
   // w's checkpoint nor its result); kept if w is clean, dropped otherwise
@@ -934,7 +937,7 @@ int none_sweep(Group& G) {
 // IPC transport: the window verdict (dirty, extent) is max-reduced over every
 // rank through the host-shared slots.  Window w's values go to parity w & 1
 // once every rank has reduced window w - 2 (nobody still reads that parity).
-int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
+int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax, std::vector<uint8_t>* F) {
   on_dev(h);
   int d[3] = {0, 0, 0};
   CK(cudaMemcpyAsync(d, &h->st->dirty, sizeof(d), cudaMemcpyDeviceToHost, h->stream));
@@ -943,12 +946,31 @@ int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
   const int n = h->cfg.nranks, me = h->cfg.rank, par = (int)(w & 1);
   for (int r = 0; r < n; ++r)
     TRY(ipc_wait(&h->shm[r].wdone, w - 2));
+  if (F) {
+    // this slab's flagged layers as bits (bit z - z_begin), beside the verdict
+    const int64_t zc = h->cfg.z_count, zb = h->cfg.z_begin;
+    uint32_t* bits = h->shm[me].zbits[par];
+    for (int64_t i = 0; i < (zc + 31) / 32; ++i) bits[i] = 0;
+    if (d[0] > 0) {
+      std::vector<int> own((size_t)zc);
+      CK(cudaMemcpyAsync(own.data(), h->zflag + zb, sizeof(int) * (size_t)zc, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      for (int64_t i = 0; i < zc; ++i)
+        if (own[(size_t)i]) bits[i >> 5] |= 1u << (i & 31);
+    }
+    F->assign((size_t)h->cfg.nz_global, 0);
+  }
   for (int k = 0; k < 3; ++k) h->shm[me].val[par][k] = d[k];
   __atomic_store_n(&h->shm[me].wseq, w, __ATOMIC_RELEASE);
   int m[3] = {0, 0, 0};
   for (int r = 0; r < n; ++r) {
     TRY(ipc_wait(&h->shm[r].wseq, w));
     for (int k = 0; k < 3; ++k) m[k] = std::max(m[k], h->shm[r].val[par][k]);
+    if (F && h->shm[r].val[par][0] > 0) {
+      const int64_t zb = h->shm[r].z_begin, zc = h->shm[r].z_count;
+      for (int64_t i = 0; i < zc; ++i)
+        if (h->shm[r].zbits[par][i >> 5] >> (i & 31) & 1u) (*F)[(size_t)(zb + i)] = 1;
+    }
   }
   __atomic_store_n(&h->shm[me].wdone, w, __ATOMIC_RELEASE);
   *dirty = m[0];
@@ -959,10 +981,10 @@ int read_dirty_ipc(abft_stencil* h, int* dirty, int64_t* zmin, int64_t* zmax) {
 
 // the last window check over every slab of the job: flagged layers (> 0:
 // dirty) and the global extent [zmin, zmax] of the flagged layers
-int read_dirty(Group& G, int* dirty, int64_t* zmin, int64_t* zmax) {
+int read_dirty(Group& G, int* dirty, int64_t* zmin, int64_t* zmax, std::vector<uint8_t>* F) {
   *dirty = 0;
   int ext[2] = {0, 0};
-  if (G.size() == 1 && G[0]->ipc) return read_dirty_ipc(G[0], dirty, zmin, zmax);
+  if (G.size() == 1 && G[0]->ipc) return read_dirty_ipc(G[0], dirty, zmin, zmax, F);
   for (abft_stencil* h : G) {
     on_dev(h);
     if (G.size() == 1 && h->cfg.nranks > 1) {
@@ -986,17 +1008,59 @@ int read_dirty(Group& G, int* dirty, int64_t* zmin, int64_t* zmax) {
   return ABFT_OK;
 }
 
+// the global layers the last window check flagged, over every slab of the
+// job (partial re-execution, Q28): each slab's check marked its own layers in
+// its zflag array (indexed by global layer).  NCCL ranks max-reduce the array
+// in place; the IPC transport carries the marks with the verdict instead
+// (read_dirty_ipc).  Called by every rank once the verdict is dirty.
+int read_flagged(Group& G, std::vector<uint8_t>* F) {
+  const int64_t nzg = G[0]->cfg.nz_global;
+  F->assign((size_t)nzg, 0);
+  std::vector<int> w((size_t)nzg);
+  for (abft_stencil* h : G) {
+    on_dev(h);
+    int64_t z0 = h->cfg.z_begin, n = h->cfg.z_count;
+    if (G.size() == 1 && h->cfg.nranks > 1) {
+      NcclApi* a = nccl_api();
+      if (!a) return ABFT_ENCCL;
+      if (a->allReduce(h->zflag, h->zflag, (size_t)nzg, ncclInt32, ncclMax, h->comm, h->stream) != ncclSuccess)
+        return ABFT_ENCCL;
+      z0 = 0;
+      n = nzg;
+    }
+    CK(cudaMemcpyAsync(w.data() + z0, h->zflag + z0, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int64_t z = z0; z < z0 + n; ++z)
+      if (w[(size_t)z]) (*F)[(size_t)z] = 1;
+  }
+  return ABFT_OK;
+}
+
+using ZRanges = std::vector<std::pair<int64_t, int64_t>>;
+// the ranges, each widened by m layers, clipped to the domain and merged
+// where they touch (ascending, disjoint)
+ZRanges widen(const ZRanges& R, int64_t m, int64_t nzg) {
+  ZRanges out;
+  for (const auto& r : R) {
+    const int64_t lo = std::max<int64_t>(0, r.first - m), hi = std::min<int64_t>(nzg - 1, r.second + m);
+    if (!out.empty() && lo <= out.back().second + 1) out.back().second = std::max(out.back().second, hi);
+    else out.push_back({lo, hi});
+  }
+  return out;
+}
+
 // Partial re-execution of a dirty window of L sweeps (recovery PARTIAL,
-// P:107-108, Q28): only the global layers [zlo, zhi]
-// are recomputed from the checkpoint.  Sweep k re-executes the light cone
-// [zlo - (L - k), zhi + (L - k)] of that range, reading sweep k - 1's cone;
-// the cone of sweep k < L goes to the two buffers other than `last` (the
-// first execution's result), ping-pong -- the checkpoint is read by sweep 1
-// only -- and sweep L writes [zlo, zhi] into `last`, whose other layers keep
-// the first execution.  The predictions P are re-advanced over the same
-// cones, the actual checksums of [zlo, zhi] recomputed and compared.
-int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, int ckgen, int gend,
-                   int64_t s0) {
+// P:107-108, Q28): only the global layers of R (ascending
+// disjoint ranges: the layers within 2 (L - 1) of a flagged one) are
+// recomputed from the checkpoint.  Sweep k re-executes the light cones of
+// those ranges -- each widened by L - k layers, merged where they meet --
+// reading sweep k - 1's cones; the cones of sweep k < L go to the two
+// buffers other than `last` (the first execution's result), ping-pong -- the
+// checkpoint is read by sweep 1 only -- and sweep L writes the ranges into
+// `last`, whose other layers keep the first execution.  The predictions P
+// are re-advanced over the same cones, the actual checksums of the ranges
+// recomputed and compared.
+int partial_window(Group& G, int L, const ZRanges& R, int ck, int last, int ckgen, int gend, int64_t s0) {
   int other = 0;
   while (other == ck || other == last) ++other;
   int src = ck;
@@ -1004,32 +1068,35 @@ int partial_window(Group& G, int L, int64_t zlo, int64_t zhi, int ck, int last, 
     const int64_t s = s0 + k;
     const bool end = k == L;
     const int dst = end ? last : (src == ck ? other : ck);
-    const int64_t glo = std::max<int64_t>(0, zlo - (L - k));
-    const int64_t ghi = std::min<int64_t>(G[0]->cfg.nz_global - 1, zhi + (L - k));
+    const ZRanges cones = widen(R, L - k, G[0]->cfg.nz_global);
     set_fwd(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, k & 1});
     for (abft_stencil* h : G) {
       const int64_t zb0 = h->cfg.z_begin;
-      const int za = (int)std::max<int64_t>(0, glo - zb0);
-      const int zb = (int)std::min<int64_t>(h->cfg.z_count, ghi - zb0 + 1);
-      if (za >= zb) { h->executed++; continue; }   // the cone misses this slab
       const double* pA = k == 1 ? h->gA[ckgen] : h->PA[(k - 1) & 1];
       const double* pB = k == 1 ? h->gB[ckgen] : h->PB[(k - 1) & 1];
-      CheckParams c;
       const bool bonly = h->cfg.checksum_policy == ABFT_CK_LAZY;   // Q29
-      if (!end) {
-        TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s, za, zb));
-        c = make_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[k & 1], h->PB[k & 1], nullptr,
-                       nullptr, CK_STORE_PRED | (bonly ? CK_BONLY : 0), s);
-      } else {
-        TRY(zero_gen(h, gend, za, zb));
-        TRY(launch_k1(h, src, dst, bonly ? nullptr : h->gA[gend], h->gB[gend], bonly ? K1_CK_B : K1_CK_AB, s,
-                      za, zb));
-        c = make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
-                       nullptr, CK_COMPARE | CK_OFFLINE_END | CK_PERSIST | (bonly ? CK_BONLY : 0), s);
+      const int64_t executed0 = h->executed;
+      for (const auto& cone : cones) {
+        const int za = (int)std::max<int64_t>(0, cone.first - zb0);
+        const int zb = (int)std::min<int64_t>(h->cfg.z_count, cone.second - zb0 + 1);
+        if (za >= zb) continue;   // the cone misses this slab
+        CheckParams c;
+        if (!end) {
+          TRY(launch_k1(h, src, dst, nullptr, nullptr, K1_CK_NONE, s, za, zb));
+          c = make_check(h, src, dst, pA, pB, nullptr, nullptr, h->PA[k & 1], h->PB[k & 1], nullptr,
+                         nullptr, CK_STORE_PRED | (bonly ? CK_BONLY : 0), s);
+        } else {
+          TRY(zero_gen(h, gend, za, zb));
+          TRY(launch_k1(h, src, dst, bonly ? nullptr : h->gA[gend], h->gB[gend], bonly ? K1_CK_B : K1_CK_AB, s,
+                        za, zb));
+          c = make_check(h, src, dst, pA, pB, h->gA[gend], h->gB[gend], nullptr, nullptr, nullptr,
+                         nullptr, CK_COMPARE | CK_OFFLINE_END | CK_PERSIST | (bonly ? CK_BONLY : 0), s);
+        }
+        c.zr0 = za;
+        c.zr1 = zb;
+        TRY(launch_check(h, c));
       }
-      c.zr0 = za;
-      c.zr1 = zb;
-      TRY(launch_check(h, c));
+      h->executed = executed0 + 1;   // one sweep, whatever the number of cones
     }
     TRY(halo_exchange(G, end ? XSpec{dst, XV_GEN, gend} : XSpec{dst, XV_P, k & 1}));
     for (abft_stencil* h : G) h->sweeps = s;
@@ -1106,11 +1173,16 @@ int offline_window(Group& G, int L, bool spec_next) {
   const bool single = G.size() == 1 && h0->cfg.nranks == 1;
   int last = ck;
   int worst = ABFT_OK;
-  int64_t zlo = 0, zhi = 0;
+  ZRanges redo;
+  std::vector<uint8_t> flagged;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    for (abft_stencil* h : G) { on_dev(h); CK(cudaMemsetAsync(&h->st->dirty, 0, 3 * sizeof(int), h->stream)); }
+    for (abft_stencil* h : G) {
+      on_dev(h);
+      CK(cudaMemsetAsync(&h->st->dirty, 0, 3 * sizeof(int), h->stream));
+      if (partial && attempt == 0) CK(cudaMemsetAsync(h->zflag, 0, sizeof(int) * (size_t)h->cfg.nz_global, h->stream));
+    }
     if (attempt == 1 && partial) {
-      TRY(partial_window(G, L, zlo, zhi, ck, last, ckgen, gend, s0));
+      TRY(partial_window(G, L, redo, ck, last, ckgen, gend, s0));
     } else {
       int src = ck;
       for (int t = 1; t <= L; ++t) {
@@ -1154,7 +1226,7 @@ int offline_window(Group& G, int L, bool spec_next) {
       if (spec) TRY(spec_sweep(h0, ck, last, gend, s0 + L + 1));
       TRY(verdict_wait(h0, &dirty, &zmin, &zmax));
     } else {
-      TRY(read_dirty(G, &dirty, &zmin, &zmax));
+      TRY(read_dirty(G, &dirty, &zmin, &zmax, partial && attempt == 0 ? &flagged : nullptr));
     }
     for (abft_stencil* h : G) h->windows++;
     if (!dirty) {
@@ -1162,17 +1234,18 @@ int offline_window(Group& G, int L, bool spec_next) {
       break;
     }
     if (spec) h0->executed--;   // the speculative sweep is dropped (it ran on a dirty result)
-    if (attempt == 0) {
-      // re-execution range of a partial recovery: every layer an error of
-      // this window that was flagged can have reached (Q28)
-      const int64_t nzg = h0->cfg.nz_global;
-      zlo = std::max<int64_t>(0, zmin - 2 * (L - 1));
-      zhi = std::min<int64_t>(nzg - 1, zmax + 2 * (L - 1));
+    if (attempt == 0 && partial) {
+      // layers a partial recovery re-executes: every layer an error of this
+      // window that was flagged can have reached -- within 2 (L - 1) layers
+      // of a flagged one (Q28)
+      if (!(G.size() == 1 && h0->ipc)) TRY(read_flagged(G, &flagged));
+      const int64_t nzg = h0->cfg.nz_global, r = 2 * (L - 1);
+      ZRanges fl;
+      for (int64_t z = 0; z < nzg; ++z)
+        if (flagged[(size_t)z]) fl.push_back({z, z});
+      redo = widen(fl, r, nzg);
       // periodic z: a reach past a face wraps to the far layers -- take them all
-      if (h0->cfg.bc == ABFT_BC_PERIODIC && (zmin - 2 * (L - 1) < 0 || zmax + 2 * (L - 1) > nzg - 1)) {
-        zlo = 0;
-        zhi = nzg - 1;
-      }
+      if (h0->cfg.bc == ABFT_BC_PERIODIC && (zmin - r < 0 || zmax + r > nzg - 1)) redo = {{0, nzg - 1}};
     }
     for (abft_stencil* h : G) {
       if (attempt == 0) {
@@ -1536,6 +1609,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   h->lazy_mark = h->lazy_rowlist + 2 * (cfg->z_count + 2);
   for (int b = 0; b < 3; ++b) h->EX[b] = h->aux + L.off_EX[b];
   h->st = reinterpret_cast<DevState*>(h->aux + L.off_st);
+  h->zflag = reinterpret_cast<int*>(h->aux + L.off_zflag);
   h->has_lo = z_ring(*cfg) || cfg->rank > 0;
   h->has_hi = z_ring(*cfg) || cfg->rank < cfg->nranks - 1;
   const int64_t nx = cfg->nx, ny = cfg->ny, zc = cfg->z_count;
@@ -1626,7 +1700,7 @@ int abft_stencil_init(const abft_config* cfg, void* const field_bufs[3], void* a
   cp.has_lo = h->has_lo; cp.has_hi = h->has_hi;
   cp.bc = cfg->bc;
   cp.g = sp.g;
-  cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st; cp.lazy_list = h->lazy_list;
+  cp.cA = h->cA; cp.cB = h->cB; cp.summ = h->summ; cp.st = h->st; cp.zflag = h->zflag; cp.lazy_list = h->lazy_list;
   cp.lazy_rowlist = h->lazy_rowlist; cp.lazy_mark = h->lazy_mark;
   cp.npoints = cfg->npoints;
   for (int q = 0; q < cfg->npoints; ++q) {
@@ -1812,6 +1886,9 @@ int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_b
     return ABFT_EINVAL;
   if ((h->has_lo != 0) != (lo_blob != nullptr) || (h->has_hi != 0) != (hi_blob != nullptr)) return ABFT_EINVAL;
   if (!h->ev_ipc[0]) return ABFT_EINVAL;   // export first (it creates the events the neighbours open)
+  // the slots carry a slab's flagged layers (partial re-execution) as bits
+  if (h->cfg.recovery == ABFT_RECOVER_PARTIAL && h->cfg.z_count > 32 * (int64_t)ABFT_IPC_ZWORDS)
+    return ABFT_EUNSUPPORTED;
   DevScope ds(h);
   const void* blobs[2] = {lo_blob, hi_blob};
   std::vector<std::pair<cudaIpcMemHandle_t, char*>> seen;
@@ -1873,6 +1950,8 @@ int abft_stencil_ipc_link(abft_stencil* h, const void* lo_blob, const void* hi_b
   h->shm = static_cast<abft_ipc_slot*>(shm);
   h->xseq = h->wseq = 0;
   memset(&h->shm[h->cfg.rank], 0, sizeof(abft_ipc_slot));
+  h->shm[h->cfg.rank].z_begin = (int32_t)h->cfg.z_begin;
+  h->shm[h->cfg.rank].z_count = (int32_t)h->cfg.z_count;
   // initial halo of u^0 and a^0, b^0: pull the neighbours' boundary layers
   // (their exports synchronised their init); their first writes into these
   // buffers come after their first sweep, which waits for this rank's

@@ -515,6 +515,7 @@ __device__ __forceinline__ void finish_layer(const CheckParams& p, int z, int na
       // the flagged layers' extent (partial re-execution, Q28)
       atomicMax(&p.st->zext[0], (int)(0x7fffffffLL - r.z));
       atomicMax(&p.st->zext[1], (int)(r.z + 1));
+      p.zflag[r.z] = 1;
     }
     return;
   }

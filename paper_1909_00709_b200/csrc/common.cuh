@@ -155,6 +155,7 @@ struct CheckParams {
   void* EXc;           // edge columns of ucur (patched by a correction)
   LayerSummary* summ;  // [zc]
   DevState* st;
+  int* zflag;          // offline window end: [nz_global], 1 for a flagged global layer (Q28)
   double* Aw;          // lazy policy: a^{s-1} written by K3 (the predictor input generation)
   void* peerU[2];      // fused halo: neighbours' halo layer of ucur (corrections), or null
   double* fwdA[2];     // fused halo: neighbours' halo row of the checksums / predictions

@@ -579,6 +579,32 @@ def test_offline_partial_slab_group(G, halo):
             assert s[k] == o["stats"][k], (k, s, o["stats"])
 
 
+@pytest.mark.parametrize("checksums", [0, 1])
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_offline_partial_union_of_cones(G, checksums, halo):
+    # the oracle pin test_partial_reexecution_is_the_union_of_the_flagged_layers_neighbourhoods
+    # at GPU scale: two clusters of flagged layers (3 and 44 of 48), an
+    # undetected flip half way -- several re-executed ranges per sweep, on
+    # one slab and across slab faces; the layers between keep the first
+    # execution, so the result equals the run with the undetected flip alone
+    from tests.parity_util import assert_records_equal
+    p = make_problem("cfg3", nx=96, ny=80, nz=48, sweeps=6, mode=2, delta=3, recovery=1, checksums=checksums)
+    lo = Fault(1, 24, 9, 9, 3)
+    faults = [Fault(1, 3, 5, 5, 29), Fault(2, 44, 20, 11, 30), lo,
+              Fault(5, 40, 70, 90, 29), Fault(4, 10, 1, 2, 30), Fault(6, 25, 33, 33, 28)]
+    o = oracle_run(p, faults=faults)
+    assert o["stats"]["rollbacks"] == 2 and o["stats"]["persistent"] == 0
+    g = _group_run(p, G, faults) if G > 1 else gpu_run(p, faults=faults)
+    assert np.array_equal(g["u"].view(np.uint32), o["u"].view(np.uint32))
+    assert_records_equal(g, o)
+    if checksums == 0:
+        assert np.array_equal(g["A"], o["A"])
+    assert np.array_equal(g["B"], o["B"])
+    only_lo = gpu_run(p, faults=[lo])
+    assert only_lo["stats"]["rollbacks"] == 0
+    assert np.array_equal(g["u"].view(np.uint32), only_lo["u"].view(np.uint32))
+
+
 @pytest.mark.parametrize("bc,z0", [(0, 8), (1, 1)])
 def test_offline_partial_reach_on_the_unflagged_side(bc, z0):
     # the oracle pin test_partial_reach_covers_errors_on_the_unflagged_side at

@@ -89,6 +89,9 @@ CASES = {
     "lazy": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=30, nfaults=8, mode=1, checksums=1),
     "offline": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=28, nfaults=8, mode=2, delta=7),
     "partial": dict(name="cfg3", nx=96, ny=80, nz=24, sweeps=18, mode=2, delta=6, recovery=1),
+    # two clusters of flagged layers far apart: the union of their cones is
+    # re-executed, an undetected flip between them is kept (Q28)
+    "partial_union": dict(name="cfg3", nx=96, ny=80, nz=48, sweeps=6, mode=2, delta=3, recovery=1),
     # offline under policy LAZY: b alone predicted, summed, compared (Q29)
     "offline_lazy": dict(name="cfg3", nx=96, ny=80, nz=12, sweeps=28, nfaults=8, mode=2, delta=7,
                          checksums=1),
@@ -105,7 +108,10 @@ CASES = {
 def test_ipc_processes_equal_oracle(world, case):
     pkw = CASES[case]
     p = make_problem(pkw["name"], **{k: v for k, v in pkw.items() if k != "name"})
-    if case.startswith("partial"):
+    if case == "partial_union":
+        faults = [Fault(1, 3, 5, 5, 29), Fault(2, 44, 20, 11, 30), Fault(1, 24, 9, 9, 3),
+                  Fault(5, 40, 70, 90, 29), Fault(4, 10, 1, 2, 30)]
+    elif case.startswith("partial"):
         faults = [Fault(1, 11, 7, 9, 24), Fault(7, 0, 79, 95, 30), Fault(13, 23, 0, 0, 28),
                   Fault(13, 5, 5, 5, 29)]
     else:

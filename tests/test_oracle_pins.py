@@ -636,6 +636,34 @@ def test_partial_reexecution_keeps_layers_no_detected_error_reached():
     assert not (part["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
 
 
+def test_partial_reexecution_is_the_union_of_the_flagged_layers_neighbourhoods():
+    # two detected flips far apart (layers 3 and 44) and, in the same window,
+    # an undetected low-bit flip half way (layer 24), outside both
+    # neighbourhoods (window of 3 sweeps: 2 * 2 layers around each flagged
+    # layer, flags at most 2 layers from a flip): only the layers near the
+    # detected flips are re-executed, so the result equals the run with the
+    # undetected flip alone -- one interval from the lowest to the highest
+    # flagged layer would have erased it as the full rollback does
+    p = make_problem("cfg3", nx=40, ny=32, nz=48, sweeps=3, mode=2, delta=3)
+    hi = [Fault(1, 3, 5, 5, 29), Fault(2, 44, 20, 11, 30)]
+    lo = Fault(1, 24, 9, 9, 3)
+    full = _offline(p, hi + [lo], 0)
+    part = _offline(p, hi + [lo], 1)
+    only_lo = _offline(p, [lo], 0)
+    clean = _offline(p, [], 0)
+    assert only_lo["stats"]["rollbacks"] == 0          # the low bit goes undetected
+    assert part["stats"]["rollbacks"] == 1 and part["stats"]["persistent"] == 0
+    zs = sorted({r["z"] for r in part["records"]})
+    assert zs and min(zs) <= 5 and max(zs) >= 42 and not any(8 <= z <= 39 for z in zs)
+    assert (full["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+    assert (part["u"].view(np.uint32) == only_lo["u"].view(np.uint32)).all()
+    assert not (part["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+    # with every flip detected the union is bitwise the full rollback
+    both = _offline(p, hi, 1)
+    assert (both["u"].view(np.uint32) == clean["u"].view(np.uint32)).all()
+    assert (both["A"] == clean["A"]).all() and (both["B"] == clean["B"]).all()
+
+
 # ------------------------------- offline, detection by b alone (Q29)
 
 @pytest.mark.parametrize("checksums", [0, 1])

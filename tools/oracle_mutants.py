@@ -95,7 +95,14 @@ MUTANTS = [
     ("offline: no rollback", "P:696-698", "if (cur != ckpt) memcpy(cur, ckpt, fb);", ""),
     ("offline: record at window start", "P:737-745", "r.sweep = wend; r.z = z;", "r.sweep = s; r.z = z;"),
     ("partial: reach L - 1", "Q28", "const int64_t r = 2 * (wend - s - 1);", "const int64_t r = (wend - s - 1);"),
-    ("partial: no periodic wrap", "Q28", "if (p->bc == OR_BC_PERIODIC && (zmin - r < 0 || zmax + r > nz - 1)) { zlo = 0; zhi = nz - 1; }", ""),
+    ("partial: no periodic wrap", "Q28", "if (p->bc == OR_BC_PERIODIC && wraps) memset(redo, 1, (size_t)nz);", ""),
+    ("partial: one interval over all flagged layers", "Q28", "memset(redo, 0, (size_t)nz);\n            for (int64_t f = 0;",
+     "memset(redo, 0, (size_t)nz);\n            { int64_t f0 = nz, f1 = -1; for (int64_t f = 0; f < nz; f++) if (flagged[f]) { if (f < f0) f0 = f; f1 = f; }\n"
+     "              for (int64_t z = f0; z <= f1; z++) redo[z] = 1; }\n            for (int64_t f = 0;"),
+    # (re-checking every layer after a partial re-execution is an equivalent
+    # mutant: the kept layers hold the values and predictions that did not
+    # flag the first time)
+    ("partial: first execution kept everywhere", "Q28", "if (!redo[z]) memcpy((char*)cur", "if (1) memcpy((char*)cur"),
     ("offline lazy: a compared", "Q29", "if (p->checksums != 1)\n            for (int64_t x = 0;", "if (1)\n            for (int64_t x = 0;"),
     ("offline: rollbacks not counted", "P:737", "stats->rollbacks++;", ";"),
 ]
