@@ -85,3 +85,60 @@ def sum_over_ranks(value: float, world: int, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+# ---- offline partial re-execution over slabs (recovery PARTIAL, Q28)
+# The library's host logic (offline_window / partial_window / widen in
+# csrc/abft_stencil.cu) stated once more so that it can be run on CPU.
+
+def flagged_over_ranks(own_layers, nz: int, world: int):
+    """The global layers any rank's window check flagged: every rank marks its
+    own layers in an array indexed by global layer, max-reduced over ranks
+    (the library: ncclMax in place, or bits in the IPC slots)."""
+    import torch
+    t = torch.zeros(nz, dtype=torch.int32)
+    for z in own_layers:
+        t[z] = 1
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [z for z in range(nz) if int(t[z])]
+
+
+def widen(ranges, m: int, nz: int) -> List[Tuple[int, int]]:
+    """Ascending inclusive ranges, each widened by m layers, clipped to the
+    domain and merged where they touch."""
+    out: List[Tuple[int, int]] = []
+    for lo, hi in ranges:
+        lo, hi = max(0, lo - m), min(nz - 1, hi + m)
+        if out and lo <= out[-1][1] + 1:
+            out[-1] = (out[-1][0], max(out[-1][1], hi))
+        else:
+            out.append((lo, hi))
+    return out
+
+
+def reexecution_ranges(flagged, L: int, nz: int, periodic: bool = False) -> List[Tuple[int, int]]:
+    """Layers a dirty window of L sweeps re-executes: within 2 (L - 1) of a
+    flagged layer (an error spreads L - 1 layers, a flag lies within that
+    reach of its origin); periodic z: everything once a reach passes a face."""
+    r = 2 * (L - 1)
+    if periodic and flagged and (min(flagged) - r < 0 or max(flagged) + r > nz - 1):
+        return [(0, nz - 1)]
+    return widen([(z, z) for z in sorted(flagged)], r, nz)
+
+
+def cones(ranges, k: int, L: int, nz: int) -> List[Tuple[int, int]]:
+    """What sweep k (1..L) of the re-execution computes: the ranges widened by
+    L - k layers, so that sweep k + 1 finds every layer it reads."""
+    return widen(ranges, L - k, nz)
+
+
+def local_pieces(rs, z0: int, zc: int) -> List[Tuple[int, int]]:
+    """The slab-local half-open pieces [za, zb) of global inclusive ranges."""
+    out = []
+    for lo, hi in rs:
+        za, zb = max(0, lo - z0), min(zc, hi - z0 + 1)
+        if za < zb:
+            out.append((za, zb))
+    return out

@@ -113,6 +113,93 @@ def test_slab_halo_protocol_reproduces_single_domain(world, nz):
     mp.spawn(_worker, args=(world, _port(), nz, 4), nprocs=world, join=True)
 
 
+def _partial_worker(rank, world, port, nz, L):
+    """One dirty offline window of L sweeps recovered by slabs: the flagged
+    layers reduced over ranks, the re-execution plan of dist.py (ranges, cones
+    per sweep, local pieces), layers outside the cones poisoned -- the result
+    must be the single-domain oracle's partial re-execution bitwise."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = make_problem("cfg3", nx=24, ny=20, nz=nz, sweeps=L, mode=2, delta=L, recovery=1)
+        u0 = field_u0(p).numpy()
+        P = field_power(p).numpy()
+        faults = [Fault(1, 2, 7, 9, 29), Fault(2, nz - 4, 3, 3, 30), Fault(1, nz // 2, 10, 10, 2)]
+        ref = O.run(O.OProblem(p, [P]), u0, L, faults)          # single domain, recovery PARTIAL
+        assert ref["stats"]["rollbacks"] == 1 and ref["stats"]["persistent"] == 0
+        first = O.run(O.OProblem(p.replace(mode=0), [P]), u0, L, faults)["u"]   # the first execution
+        flagged_ref = sorted(r["z"] for r in ref["records"])
+
+        z0, zc = D.slab(nz, world, rank)
+        flagged = D.flagged_over_ranks([z for z in flagged_ref if z0 <= z < z0 + zc], nz, world)
+        assert flagged == flagged_ref
+        ranges = D.reexecution_ranges(flagged, L, nz)
+        assert len(ranges) == 2                                  # two clusters, far apart
+        r = 2 * (L - 1)
+        inside = lambda z, rs: any(lo <= z <= hi for lo, hi in rs)
+        assert all(inside(z, ranges) == any(abs(z - f) <= r for f in flagged) for z in range(nz))
+
+        lo, hi = D.neighbours(rank, world)
+        plan = D.halo_plan(rank, world, zc)
+        ue = np.zeros((zc + 2, p.ny, p.nx), np.float32)
+        ue[1:zc + 1] = u0[z0:z0 + zc]
+        Pe = P[[min(max(z, 0), nz - 1) for z in range(z0 - 1, z0 + zc + 1)]]
+        ope = O.OProblem(p.replace(nz=zc + 2, mode=0), [Pe])
+
+        def halo():
+            def send(peer, layer):
+                dist.send(torch.from_numpy(ue[layer].copy()), peer)
+
+            def recv(peer, layer):
+                t = torch.empty((p.ny, p.nx), dtype=torch.float32)
+                dist.recv(t, peer)
+                ue[layer] = t.numpy()
+
+            D.exchange(rank, plan, send, recv)
+            if lo is None:
+                ue[0] = ue[1]
+            if hi is None:
+                ue[zc + 1] = ue[zc]
+
+        halo()
+        for k in range(1, L + 1):
+            cs = D.cones(ranges, k, L, nz)
+            assert all(inside(z, cs) == any(lo_ - (L - k) <= z <= hi_ + (L - k) for lo_, hi_ in ranges)
+                       for z in range(nz))
+            un = O.sweep(ope, ue, k, [])                         # transient faults do not strike again
+            nxt = np.full_like(ue, np.nan)                       # layers outside the cones: never read
+            for za, zb in D.local_pieces(cs, z0, zc):
+                nxt[1 + za:1 + zb] = un[1 + za:1 + zb]
+            ue = nxt
+            halo()
+        out = first[z0:z0 + zc].copy()
+        for za, zb in D.local_pieces(ranges, z0, zc):
+            out[za:zb] = ue[1 + za:1 + zb]
+        assert np.array_equal(out.view(np.uint32), ref["u"][z0:z0 + zc].view(np.uint32)), rank
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nz", [(2, 32), (3, 31)])
+def test_partial_reexecution_plan_over_slabs(world, nz):
+    mp.spawn(_partial_worker, args=(world, _port(), nz, 3), nprocs=world, join=True)
+
+
+def test_reexecution_ranges_and_cones():
+    assert D.widen([(3, 3), (5, 5), (20, 21)], 1, 24) == [(2, 6), (19, 22)]
+    assert D.widen([(0, 0), (23, 23)], 4, 24) == [(0, 4), (19, 23)]
+    assert D.reexecution_ranges([3, 44], 3, 48) == [(0, 7), (40, 47)]
+    assert D.reexecution_ranges([3, 11], 3, 48) == [(0, 15)]              # neighbourhoods meet
+    assert D.reexecution_ranges([10], 1, 48) == [(10, 10)]                # L = 1: the layer alone
+    assert D.reexecution_ranges([3, 30], 3, 48, periodic=True) == [(0, 47)]
+    assert D.reexecution_ranges([10, 30], 3, 48, periodic=True) == [(6, 14), (26, 34)]
+    assert D.cones([(0, 7), (40, 47)], 1, 3, 48) == [(0, 9), (38, 47)]
+    assert D.cones([(6, 14), (18, 20)], 1, 3, 48) == [(4, 22)]            # cones merge, ranges do not
+    assert D.local_pieces([(0, 9), (38, 47)], 8, 32) == [(0, 2), (30, 32)]
+    assert D.local_pieces([(0, 9)], 16, 8) == []
+
+
 def test_partition_and_plan():
     for nz, world in [(1024, 8), (11, 3), (7, 7), (1000, 3)]:
         parts = [D.slab(nz, world, r) for r in range(world)]
