@@ -312,8 +312,10 @@ int abft_stencil_step_group(abft_stencil* const* hs, int32_t n, int32_t nsweeps)
  * over all ranks through the slots.  Every rank
  * calls step() with the same counts (lockstep).  Errors: ABFT_EINVAL for a
  * handle that is grouped, has a communicator, has stepped, or a blob that
- * does not describe the expected neighbour; ABFT_ECUDA if a handle or event
- * cannot be opened. */
+ * does not describe the expected neighbour; ABFT_EUNSUPPORTED for recovery
+ * PARTIAL with a slab of more than 32 * ABFT_IPC_ZWORDS layers (its flagged
+ * layers travel as bits in the slot); ABFT_ECUDA if a handle or event cannot
+ * be opened. */
 #define ABFT_IPC_BLOB_BYTES 1024
 #define ABFT_IPC_ZWORDS 256   /* recovery PARTIAL over IPC: z_count <= 32 * ABFT_IPC_ZWORDS per rank */
 typedef struct {
