@@ -11,3 +11,5 @@ ABFT_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --
 done
 timeout 1800 python campaign.py --exp e1,e3 --reps 20 --out gpurun_out/campaign.json > gpurun_out/campaign.log 2>&1; echo campaign_rc=$?
 python tools/campaign_summary.py gpurun_out/campaign.json > gpurun_out/campaign_summary.md 2>&1
+# recovery of dirty offline windows on the cfg5 slab: ROLLBACK vs PARTIAL, 1-4 flips per window
+timeout 600 python tools/exp_partial.py 3 > gpurun_out/exp_partial.txt 2>&1; echo exp_partial_rc=$?
