@@ -200,6 +200,34 @@ def test_reexecution_ranges_and_cones():
     assert D.local_pieces([(0, 9)], 16, 8) == []
 
 
+def test_reexecution_plan_against_brute_force():
+    # random flagged sets: the ranges are exactly the layers within 2 (L - 1)
+    # of a flag, ascending, disjoint and not adjacent; sweep k's cones are
+    # exactly the layers within L - k of a range; the slabs' pieces tile them
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        nz = int(rng.integers(1, 70))
+        L = int(rng.integers(1, 7))
+        flagged = sorted(set(int(z) for z in rng.integers(0, nz, size=int(rng.integers(1, 6)))))
+        rs = D.reexecution_ranges(flagged, L, nz)
+        want = {z for z in range(nz) if any(abs(z - f) <= 2 * (L - 1) for f in flagged)}
+        assert {z for lo, hi in rs for z in range(lo, hi + 1)} == want
+        assert all(a[1] + 1 < b[0] for a, b in zip(rs, rs[1:])) and all(lo <= hi for lo, hi in rs)
+        for k in range(1, L + 1):
+            cs = D.cones(rs, k, L, nz)
+            cw = {z for z in range(nz) if any(lo - (L - k) <= z <= hi + (L - k) for lo, hi in rs)}
+            assert {z for lo, hi in cs for z in range(lo, hi + 1)} == cw
+            world = int(rng.integers(1, min(nz, 5) + 1))
+            got = set()
+            for r in range(world):
+                z0, zc = D.slab(nz, world, r)
+                for za, zb in D.local_pieces(cs, z0, zc):
+                    assert 0 <= za < zb <= zc
+                    got |= {z0 + z for z in range(za, zb)}
+            assert got == cw
+        assert D.cones(rs, L, L, nz) == rs
+
+
 def test_partition_and_plan():
     for nz, world in [(1024, 8), (11, 3), (7, 7), (1000, 3)]:
         parts = [D.slab(nz, world, r) for r in range(world)]
